@@ -1,0 +1,106 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden/).
+
+The fixtures were produced by tests/golden/make_golden.py running the
+unmodified reference; inputs are regenerated here from the same seeds and
+their checksums compared first, so an RNG-stream drift fails loudly.
+"""
+import numpy as np
+import pytest
+
+from oracle import spsim_oracle as O
+
+G = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "golden.npz"))
+DATA_TAG = 1 << 20
+BLOCK_CASES = [
+    ("blk_tiny", 4, 64, 32, 256, 4),
+    ("blk_small", 3, 5, 2, 12, 4),
+    ("blk_odd", 2, 7, 3, 18, 3),
+    ("blk_dh66", 2, 24, 8, 132, 2),
+]
+MODEL_CASES = [
+    ("cfg1", 2501, 4, 16, 16, 32, 256, 4, 2, 37),
+    ("mdl_ragged", 7, 3, 5, 7, 3, 12, 6, 1, 11),
+]
+
+
+def block_case(name, F, Lv, Lt, D):
+    seed = sum(map(ord, name))
+    blk = O.BlockParams.init(O.SeededRng(seed).split(1000), D)
+    data = O.SeededRng(seed).split(DATA_TAG)
+    x = data.split(1).normal((F, Lv, D))
+    prompt = data.split(2).normal((Lt, D))
+    return blk, x, prompt
+
+
+def test_rng_streams_bitwise():
+    assert np.array_equal(O.SeededRng(123456789).normal(64), G["rng_normal_head"])
+    assert np.array_equal(O.SeededRng(42).split(1000).split(101).normal(16), G["rng_split_head"])
+
+
+def test_attention_known_answers():
+    q, k, v = G["attn_q"], G["attn_k"], G["attn_v"]
+    for h in (1, 2, 4):
+        np.testing.assert_allclose(O.attention(q, k, v, h), G[f"attn_out_h{h}"], atol=1e-12)
+    np.testing.assert_allclose(O.softmax_rows(np.array([[0.0, np.log(3.0)]])), [[0.25, 0.75]], atol=1e-12)
+    np.testing.assert_allclose(G["softmax_pair"], [[0.25, 0.75]], atol=1e-12)
+
+
+@pytest.mark.parametrize("case", BLOCK_CASES, ids=[c[0] for c in BLOCK_CASES])
+def test_block_branches_match_reference(case):
+    name, F, Lv, Lt, D, H = case
+    blk, x, prompt = block_case(name, F, Lv, Lt, D)
+    assert np.array_equal(np.array([x.sum(), prompt.sum(), blk.fullseq.wo.sum()]), G[f"{name}_xsum"])
+    text = O.anchor_text(prompt, F)
+    np.testing.assert_allclose(O.spatial_branch(blk.spatial, x, H), G[f"{name}_sp"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(O.temporal_branch(blk.temporal, x, H), G[f"{name}_tm"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(O.full_sequence_attention(blk.fullseq, text, x, H), G[f"{name}_fs"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(O.parallel_block_forward(blk, x, text, H), G[f"{name}_out"], atol=1e-12, rtol=0)
+    # the deduplicated-text restatement (what the CUDA path computes)
+    np.testing.assert_allclose(O.full_sequence_attention_dedup(blk.fullseq, text, x, H), G[f"{name}_fs"], atol=1e-12, rtol=0)
+
+
+@pytest.mark.parametrize("case", MODEL_CASES, ids=[c[0] for c in MODEL_CASES])
+def test_model_forward_matches_reference(case):
+    name, seed, F, h, w, Lt, D, H, depth, t = case
+    model = O.ToyDenoiser.init(O.SeededRng(seed), O.PatchSpec(8, 2, 4), D, H, depth)
+    data = O.SeededRng(seed).split(DATA_TAG)
+    lat = data.split(1).normal((F, h, w, 4))
+    prompt = data.split(2).normal((Lt, D))
+    assert np.array_equal(np.array([lat.sum(), prompt.sum(), model.w_out.sum()]), G[f"{name}_xsum"])
+    np.testing.assert_allclose(model.embed_frame(lat[0], 0, t), G[f"{name}_embed0"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(model.head_states(lat, t, prompt), G[f"{name}_states"], atol=1e-11, rtol=0)
+    np.testing.assert_allclose(model.forward(lat, t, prompt), G[f"{name}_out"], atol=1e-11, rtol=0)
+
+
+def test_contiguous_bounds_exact():
+    flat = G["cb_flat"]
+    pos = 0
+    for n, p in G["cb_np"]:
+        b = O.contiguous_bounds(int(n), int(p))
+        assert np.array_equal(np.array(b), flat[pos:pos + p + 1])
+        pos += p + 1
+    assert pos == flat.size
+
+
+def test_placement_division_exact():
+    for row in G["pd_rows"]:
+        lt, lv, p, fused = (int(v) for v in row[:4])
+        tc, vc = O.placement_division(lt, lv, p, "fused" if fused else "separate")
+        assert list(row[4:4 + p]) == tc
+        assert list(row[4 + p:4 + 2 * p]) == vc
+    assert [len(d) for d in O.round_robin_frames(10, 4)] == list(G["rr_10_4"])
+
+
+def test_reference_sp_equals_single_device():
+    # acceptance criterion 1 recorded from the reference executor itself
+    for p in (2, 3):
+        np.testing.assert_allclose(G[f"sp_p{p}_pred"], G["sp_ref_pred"], atol=1e-9, rtol=0)
+
+
+def test_patchify_round_trip_and_order():
+    lat = np.arange(4 * 6, dtype=float).reshape(4, 6, 1)
+    tok = O.patchify(lat, 2)
+    assert np.array_equal(tok[1 * 3 + 2], lat[2:4, 4:6].reshape(4))
+    r = O.SeededRng(2).normal((5, 3, 2))
+    assert np.array_equal(O.unpatchify(O.patchify(r, 2), 5, 3, 2, 2), r)
+    assert O.seq_len(144, 1920, 1080) == 1_175_040
