@@ -1,0 +1,364 @@
+"""Benchmark: video tokens/s per denoise step of the Vchitect-2.0 2B block (bf16).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 2]
+
+One "step" = one parallel MM-DiT block forward (model.py:263-271) over the
+config's synthetic clip. N=1: BASELINE.json configs[1] (config 2: 16 frames x
+30x45 patches + 256 text tokens, D 1584, H 24, bf16) on one B200, inputs
+resident in HBM. N>1 (torchrun, one rank per GPU, NCCL): the same block
+sequence-parallel (spatial shard axis, head-parallel all-to-all), strong
+scaling, time = max over ranks.
+
+Rank 0 prints ONE JSON line (contract in the task statement). Extra keys:
+roofline (dominant kernel, from the library's per-stage CUDA-event profiler
+in a separate untimed pass), cpu_baseline (the oracle port on this host's
+cores, bounded sample), e2e (C-ABI call with pinned HOST buffers: H2D of the
+inputs and D2H of the block output inside the timed region), clocks.
+
+--impl reference times the reference algorithm's CPU implementation (the
+pinned oracle port, oracle/spsim_oracle.py; the reference is pure Python and
+cannot travel to the GPU box) on the same config, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # id: (F, Lv, Lt, D, H, name)
+    1: (4, 64, 32, 256, 4, "config1 tiny MM-DiT block (4 frames x 8x8 patches + 32 text, D256 H4)"),
+    2: (16, 1350, 256, 1584, 24, "config2 Vchitect-2.0 2B block (16 frames x 30x45 patches + 256 text, D1584 H24)"),
+    4: (160, 1350, 256, 1584, 24, "config4 long video 2B block (160 frames x 30x45 + 256 text)"),
+    5: (64, 256, 256, 3072, 24, "config5 temporal-dominant block (64 frames x 16x16 + 256 text, D3072 H24)"),
+}
+METRIC = "video tokens/sec per denoise step (2B block, bf16)"
+
+
+def algorithmic_flops(F, Lv, Lt, D, H):
+    """per-kernel algorithmic FLOPs (no padding, text keys deduplicated)."""
+    Nv = F * Lv
+    return {
+        "qkv_gemm": 2.0 * D * (9 * D * Nv + 2 * D * Lt),
+        "attn_spatial": 4.0 * F * Lv * Lv * D,
+        "attn_temporal": 4.0 * Lv * F * F * D,
+        "attn_fullseq": 4.0 * Nv * (Nv + Lt) * D,
+        "oproj_gemm": 2.0 * Nv * 3 * D * D,
+    }
+
+
+def algorithmic_bytes(F, Lv, Lt, D, H):
+    Nv = F * Lv
+    return {"ln": (Nv + Lt) * D * (4 + 2)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm": d.get("hbm_gbs", 6650.0), "tc": d.get("bf16_tflops", 1590.0),
+                "tc_sus": d.get("bf16_tflops_sustained", 1400.0), "src": "measured"}
+    return {"hbm": 6650.0, "tc": 1590.0, "tc_sus": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown"]
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the pinned oracle port (fp64 numpy) on a bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_sample(cfg_id, sample_frames):
+    """Time the reference algorithm (oracle port) for a `sample_frames`-frame
+    clip of the config's geometry, branch by branch, and extrapolate to the
+    full clip with the reference's own cost scaling (spatial
+    and temporal proportional to F, full sequence to S^2, S = F (Lt + Lv))."""
+    from oracle import spsim_oracle as O
+    F, Lv, Lt, D, H, _ = CONFIGS[cfg_id]
+    Fs = min(sample_frames, F)
+    blk = O.BlockParams.init(O.SeededRng(2025).split(1000), D)
+    data = O.SeededRng(2025).split(1 << 20)
+    x = data.split(1).normal((Fs, Lv, D))
+    text = O.anchor_text(data.split(2).normal((Lt, D)), Fs)
+    t0 = time.perf_counter()
+    O.spatial_branch(blk.spatial, x, H)
+    t1 = time.perf_counter()
+    O.temporal_branch(blk.temporal, x, H)
+    t2 = time.perf_counter()
+    O.full_sequence_attention(blk.fullseq, text, x, H)
+    t3 = time.perf_counter()
+    sp, tm, fs = t1 - t0, t2 - t1, t3 - t2
+    scale_f = F / Fs
+    s_ratio = (F * (Lt + Lv)) / (Fs * (Lt + Lv))
+    full = sp * scale_f + tm * scale_f + fs * s_ratio ** 2
+    return {"sample_s": t3 - t0, "full_s": full, "tokens": F * Lv,
+            "value": F * Lv / full, "branches_s": [sp, tm, fs], "Fs": Fs}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    F, Lv, Lt, D, H, name = cfg
+    for _ in range(args.warmup):
+        cpu_sample(args.config, args.sample_frames)
+    vals, samples = [], []
+    for _ in range(args.steps):
+        r = cpu_sample(args.config, args.sample_frames)
+        vals.append(r["value"])
+        samples.append(r)
+    value = float(np.median(vals))
+    full_s = float(np.median([r["full_s"] for r in samples]))
+    sample = (f"oracle port (fp64 numpy, pinned to the reference's golden outputs) block forward of a "
+              f"{samples[0]['Fs']}-frame clip of {name}, branches timed and extrapolated to F={F} "
+              f"(spatial,temporal ~F; full-sequence ~S^2); median of {args.steps} steps")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": full_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SeededRng)",
+        "config": {"workload": name, "frames": F, "visual_len": Lv, "text_len": Lt, "dim": D,
+                   "heads": H},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def make_inputs(torch, cfg_id, D, H, dtype, seed=2025):
+    import paper_2501_08453_b200 as vc
+    from paper_2501_08453_b200.model import DeviceBlock
+    F, Lv, Lt = CONFIGS[cfg_id][:3]
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    blk = vc.BlockParams.init(vc.SeededRng(seed).split(1000), D)  # random-init 2B-shape weights
+    db = DeviceBlock(torch, blk, H, dtype)
+    x = torch.randn((F, Lv, D), device="cuda", generator=g)
+    prompt = torch.randn((Lt, D), device="cuda", generator=g)
+    return db, x, prompt
+
+
+def stage_profile(torch, lib, fwd, reps):
+    lib.vc_profile_reset()
+    lib.vc_profile_enable(1)
+    for _ in range(reps):
+        fwd()
+    torch.cuda.synchronize()
+    lib.vc_profile_enable(0)
+    ms = (C.c_double * 32)()
+    calls = (C.c_int32 * 32)()
+    names = C.create_string_buffer(2048)
+    n = lib.vc_profile_read(ms, calls, 32, names, 2048)
+    out = {}
+    for i, nm in enumerate(names.value.decode().split("\n")[:n]):
+        out[nm] = ms[i] / max(calls[i], 1)
+    return out
+
+
+def run_gpu_arm(args):
+    import torch
+    import paper_2501_08453_b200 as vc  # noqa: F401
+    from paper_2501_08453_b200 import _lib
+    from paper_2501_08453_b200.model import block_forward_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        return run_gpu_sp(args, torch, world, rank, local)
+
+    lib = _lib.load()
+    F, Lv, Lt, D, H, name = CONFIGS[args.config]
+    Nv = F * Lv
+    db, x, prompt = make_inputs(torch, args.config, D, H, args.dtype)
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def fwd():
+        block_forward_device(torch, db, x, prompt, out, False)
+
+    for _ in range(max(args.warmup, 3)):
+        fwd()
+    torch.cuda.synchronize()
+    # ---- timed region (device, CUDA events on the launching stream) ----
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            fwd()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_per_step = e0.elapsed_time(e1) / args.steps
+    value = Nv / (ms_per_step / 1e3)
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    shp = _lib.shape(F, Lv, Lt, D, H, args.dtype)
+    hws = lib.vc_block_host_workspace_bytes(C.byref(shp))
+    ws = torch.empty(hws, dtype=torch.uint8, device="cuda")
+    xh = x.cpu().pin_memory()
+    ph = prompt.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+
+    def fwd_host():
+        _lib.check(lib.vc_block_forward_host(C.byref(shp), _lib.ptr(db.packed), C.c_void_p(xh.data_ptr()),
+                                             C.c_void_p(ph.data_ptr()), C.c_void_p(oh.data_ptr()),
+                                             _lib.ptr(ws), hws, _lib.stream_ptr(torch)), "forward_host")
+
+    for _ in range(3):
+        fwd_host()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        fwd_host()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    assert torch.isfinite(oh).all().item()
+
+    # ---- per-stage device time (separate, untimed pass) ----
+    stages = stage_profile(torch, lib, fwd, max(2, min(args.steps, 5)))
+    flops = algorithmic_flops(F, Lv, Lt, D, H)
+    peaks = load_peaks()
+    dom = max((k for k in stages if k in flops), key=lambda k: stages[k])
+    achieved = flops[dom] / (stages[dom] / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"cfg{args.config}_{args.dtype}", {}).get(dom)
+    block_tflops = sum(flops.values()) / (ms_per_step / 1e3) / 1e12
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        r = cpu_sample(args.config, args.sample_frames)
+        cpu = {"value": r["value"], "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+               "sample": (f"oracle port (fp64 numpy, pinned to reference golden outputs), {r['Fs']}-frame clip "
+                          f"of the same geometry ({r['sample_s']:.1f} s), branches extrapolated to F={F} "
+                          f"(spatial,temporal ~F; full-seq ~S^2)")}
+
+    launches = lib.vc_block_forward_launches(C.byref(shp)) * args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (torch.randn inputs, SeededRng random-init 2B-shape weights)",
+        "config": {"workload": name, "frames": F, "visual_len": Lv, "text_len": Lt, "dim": D,
+                   "heads": H, "tokens_per_step": Nv, "parallelism": "single GPU",
+                   "l2": "inputs larger than L2 (x fp32 %.0f MB + weights %.0f MB > 126 MB)"
+                   % (Nv * D * 4 / 1e6, db.packed.numel() / 1e6)},
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["tc_sus"],
+                     "unit": "TFLOP/s", "frac": achieved / peaks["tc_sus"], "traffic": traffic,
+                     "peak_kind": f"{peaks['src']} bf16 sustained (kernel timed inside a long step)",
+                     "share_of_step": stages[dom] / sum(stages.values())},
+        "block": {"tflops_algorithmic": block_tflops, "frac_of_bf16_peak": block_tflops / peaks["tc"],
+                  "stage_ms": stages},
+        "cpu_baseline": cpu,
+        "e2e": {"value": Nv / (e2e_ms / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": (Nv + Lt) * D * 4, "d2h_bytes_per_step": Nv * D * 4},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu_sp(args, torch, world, rank, local):
+    from paper_2501_08453_b200 import sp
+    return sp.bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops,
+                       load_peaks, ClockSampler, cpu_sample, cpu_cores)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--sample-frames", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

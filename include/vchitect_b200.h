@@ -1,0 +1,164 @@
+/*
+ * vchitect_b200.h -- C ABI of the B200-native parallel MM-DiT block forward.
+ *
+ * Drop-in boundary for the hot path of arXiv 2501.08453 (Vchitect-2.0) as
+ * implemented by the reference CPU simulator `spsim`. Every entry point below
+ * names the reference function it replaces (paths relative to
+ * /root/reference/pkg/src/spsim/). The reference is a Python/numpy API with
+ * no FFI; the binding a maintainer would add on the reference side (ctypes)
+ * is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. "dev" pointers are CUDA device memory,
+ *     "host" pointers are host memory (pinned for async copies).
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*), never synchronises the device, never allocates device memory:
+ *     callers own the weight and workspace buffers (sizes from *_bytes()).
+ *   - Return VC_OK (0) or a negative code; vc_last_error() gives a message
+ *     (thread-local). Shape / divisibility violations return VC_EINVAL with
+ *     the reference's ValueError wording.
+ *   - Thread-safe across distinct streams and buffers.
+ *   - Weight layout in (`raw`) is the reference's BranchParams layout:
+ *     per branch gamma[D], beta[D], wq, wk, wv, wo each [D_in][D_out]
+ *     row-major (applied as x @ W, model.py:157-184); a block is the three
+ *     branches in order spatial, temporal, fullseq (model.py:193-205).
+ */
+#ifndef VCHITECT_B200_H
+#define VCHITECT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VC_API __attribute__((visibility("default")))
+#else
+#define VC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VC_OK 0
+#define VC_EINVAL (-22)
+#define VC_ECUDA (-1000)
+#define VC_ENOTSUP (-95)
+
+/* arithmetic of the path: fp32 (SIMT FFMA, the 1e-4 parity path) or bf16
+ * operands with fp32 accumulation on tcgen05 tensor cores. */
+#define VC_DTYPE_F32 0
+#define VC_DTYPE_BF16 1
+
+typedef struct vc_block_shape {
+  int32_t frames;     /* F  */
+  int32_t visual_len; /* Lv visual tokens per frame */
+  int32_t text_len;   /* Lt prompt tokens (anchored to every frame) */
+  int32_t dim;        /* D  */
+  int32_t heads;      /* H, D % H == 0 */
+  int32_t dtype;      /* VC_DTYPE_* */
+} vc_block_shape;
+
+/* Library build/version string, e.g. "vchitect_b200 sm_100a ...". */
+VC_API const char* vc_version(void);
+
+/* Message of the last failing call on this thread. */
+VC_API const char* vc_last_error(void);
+
+/* Validate a shape (model.py:263-271 preconditions; numerics.py:93-99). */
+VC_API int vc_block_shape_check(const vc_block_shape* shape);
+
+/* Element count of one block's raw fp32 weights: 3 * (2*D + 4*D*D). */
+VC_API size_t vc_block_raw_weight_floats(const vc_block_shape* shape);
+
+/* Bytes of one block's packed device weights (gamma folded into W,
+ * beta@W bias, Q/K/V of the three branches concatenated, O weights stacked). */
+VC_API size_t vc_block_packed_weight_bytes(const vc_block_shape* shape);
+
+/* Bytes of device workspace vc_block_forward needs. */
+VC_API size_t vc_block_workspace_bytes(const vc_block_shape* shape);
+
+/* Pack raw fp32 device weights (reference layout, see above) into the
+ * device layout the kernels consume. Replaces nothing in the reference
+ * (weights are used as-is there); it is the one-time load step. */
+VC_API int vc_pack_block_weights(const vc_block_shape* shape, const float* raw_dev,
+                          void* packed_dev, void* stream);
+
+/* Block forward.  Replaces parallel_block_forward (model.py:263-271) and,
+ * with add_residual=1, one iteration of ToyDenoiser.head_states'
+ * `x = x + block(x)` (model.py:323-324).
+ *   visual_dev [F][Lv][D] fp32, prompt_dev [Lt][D] fp32 (= text[0]; the
+ *   reference anchors every frame's text slots to it, model.py:257),
+ *   out_dev [F][Lv][D] fp32 (may alias visual_dev when add_residual=1). */
+VC_API int vc_block_forward(const vc_block_shape* shape, const void* packed_dev,
+                     const float* visual_dev, const float* prompt_dev,
+                     float* out_dev, int add_residual, void* workspace_dev,
+                     size_t workspace_bytes, void* stream);
+
+/* Same as vc_block_forward with HOST buffers: copies visual/prompt in,
+ * runs, copies out back, all on `stream` (the call does not synchronise;
+ * the caller syncs before reading out_host). Staging buffers for the
+ * device-side copies are carved from the workspace; size with
+ * vc_block_host_workspace_bytes(). */
+VC_API size_t vc_block_host_workspace_bytes(const vc_block_shape* shape);
+VC_API int vc_block_forward_host(const vc_block_shape* shape, const void* packed_dev,
+                          const float* visual_host, const float* prompt_host,
+                          float* out_host, void* workspace_dev,
+                          size_t workspace_bytes, void* stream);
+
+/* Multi-head attention, numerics.py:87-107: q [sq][D], k/v [sk][D] fp32
+ * device, heads contiguous column slices, scale 1/sqrt(D/heads), non-causal.
+ * fp32 SIMT path (parity 1e-4 class). */
+VC_API int vc_attention_f32(const float* q_dev, const float* k_dev, const float* v_dev,
+                     float* out_dev, int32_t sq, int32_t sk, int32_t dim,
+                     int32_t heads, void* stream);
+
+/* LayerNorm without affine, model.py:89-92 (biased var, eps 1e-5):
+ * rows x [rows][D] fp32 -> out fp32. */
+VC_API int vc_layer_norm_f32(const float* x_dev, float* out_dev, int64_t rows,
+                      int32_t dim, void* stream);
+
+/* ToyDenoiser.embed_frame for all frames, model.py:303-314 + patchify
+ * model.py:53-64: latents [F][h][w][c] fp32, w_in [p*p*c][D] fp32 ->
+ * x [F][Lv][D] fp32 (+ sinusoid of global token index (first_frame+f)*Lv+i
+ * and of t). */
+VC_API int vc_embed_frames(const float* latents_dev, const float* w_in_dev,
+                    float* x_dev, int32_t frames, int32_t first_frame,
+                    int32_t h, int32_t w, int32_t c, int32_t patch,
+                    int32_t dim, double t, void* stream);
+
+/* ToyDenoiser.forward's output projection + unpatchify crop,
+ * model.py:331-333 + model.py:67-76: x [F][Lv][D], w_out [D][p*p*c] ->
+ * eps [F][h][w][c] fp32. */
+VC_API int vc_unembed_frames(const float* x_dev, const float* w_out_dev,
+                      float* eps_dev, int32_t frames, int32_t h, int32_t w,
+                      int32_t c, int32_t patch, int32_t dim, void* stream);
+
+/* The tcgen05 GEMM on its own: out[m][n] = sum_k A[m][k] B[n][k]
+ * (+ bias[n]) (+ resid[m][n]), A/B bf16 K-major (row pitch lda/ldb elements,
+ * 16-byte aligned), fp32 accumulation and output. The projection GEMMs of the
+ * block (model.py:184, :190) run through this kernel with fused epilogues. */
+VC_API int vc_gemm_bf16(const void* a_dev, int64_t lda, const void* b_dev,
+                        int64_t ldb, const float* bias_dev,
+                        const float* resid_dev, float* out_dev, int64_t ldo,
+                        int64_t M, int32_t N, int32_t K, void* stream);
+
+/* Stage profiler (bench accounting, not used on the timed path): when
+ * enabled, vc_block_forward records a CUDA event after each of its kernels,
+ * synchronises at the end of the call and accumulates per-stage device time
+ * by stage name ("ln", "qkv_gemm", "attn_spatial", ...). */
+VC_API int vc_profile_enable(int on);
+VC_API void vc_profile_reset(void);
+/* Fills up to max_stages entries; names is a '\n'-joined list written into
+ * names_buf. Returns the number of stages. */
+VC_API int vc_profile_read(double* ms_total, int32_t* calls, int32_t max_stages,
+                           char* names_buf, size_t names_len);
+
+/* Number of kernel launches vc_block_forward issues for `shape` (the
+ * bench's gpu_launches accounting). */
+VC_API int vc_block_forward_launches(const vc_block_shape* shape);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VCHITECT_B200_H */

@@ -1,0 +1,368 @@
+// bf16 GEMM on the 5th-generation tensor cores (tcgen05) for sm_100a.
+//
+//   C[M][N] = A[M][K] . B[N][K]^T     (bf16 operands, fp32 accumulation)
+//
+// Both operands K-major (row pitch = K), fed by TMA (cp.async.bulk.tensor,
+// 128B swizzle) into a 4-stage shared-memory ring; one elected thread issues
+// tcgen05.mma (M=128, N=BN, K=16) into a double-buffered TMEM accumulator so
+// the epilogue of tile i overlaps the MMAs of tile i+1. Persistent: one CTA
+// per SM walking a static tile schedule.
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM owner,
+// w3 idle, w4..w7 epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
+//
+// Epilogues (the fused work of the block forward, model.py:181-190,:324):
+//   EPI_F32      out fp32 = acc (+ bias[n]) (+ R[m][n])   O-projection+residual
+//   EPI_BF16     out bf16 = acc + bias[n]                   plain projection
+//   EPI_QKV      acc + bias scattered into the attention layouts: Q/K
+//                [row][H][DP] (head dim zero-padded to DP), V transposed per
+//                sequence [seq][H][DP][keys] (the K-major B operand of P.V),
+//                temporal branch plain [row][3D].
+#include "vc_gemm_tc.h"
+#include "vc_ptx.cuh"
+
+namespace vc {
+
+namespace {
+constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int kThreads = 256;
+
+template <int BN>
+constexpr size_t smem_bytes() {
+  return (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 /*barriers*/ + 1024 /*align*/;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m, int n0,
+                                               const uint32_t (&r)[16]) {
+  if (m >= p.M) return;
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    v[j] = __uint_as_float(r[j]);
+    const int n = n0 + j;
+    if (p.bias && n < p.N) v[j] += __ldg(p.bias + n);
+  }
+  if constexpr (EPI == EPI_F32) {
+    float* o = p.out_f32 + m * p.ldo + n0;
+    const float* R = p.R ? p.R + m * p.ldr + n0 : nullptr;
+    if (n0 + 16 <= p.N && (p.ldo % 4) == 0 && (!R || (p.ldr % 4) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        float4 w = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if (R) {
+          float4 rr = *reinterpret_cast<const float4*>(R + j);
+          w.x += rr.x; w.y += rr.y; w.z += rr.z; w.w += rr.w;
+        }
+        *reinterpret_cast<float4*>(o + j) = w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n0 + j < p.N) o[j] = v[j] + (R ? R[j] : 0.f);
+    }
+  } else if constexpr (EPI == EPI_BF16) {
+    __nv_bfloat16* o = p.out_bf16 + m * p.ldo + n0;
+    if (n0 + 16 <= p.N && (p.ldo % 8) == 0) {
+      uint4 a, b;
+      a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);
+      a.z = pack_bf16x2(v[4], v[5]); a.w = pack_bf16x2(v[6], v[7]);
+      b.x = pack_bf16x2(v[8], v[9]); b.y = pack_bf16x2(v[10], v[11]);
+      b.z = pack_bf16x2(v[12], v[13]); b.w = pack_bf16x2(v[14], v[15]);
+      reinterpret_cast<uint4*>(o)[0] = a;
+      reinterpret_cast<uint4*>(o)[1] = b;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n0 + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {  // EPI_QKV
+    const QkvScatter& s = p.qkv;
+    const int64_t D = s.D;
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const int nl = n0 + j;
+      if (nl >= p.N) break;
+      const int64_t n = nl + s.n_base;  // column in the 9D space
+      const int b = (int)(n / (3 * D));
+      const int which = (int)((n / D) % 3);
+      const int c = (int)(n % D);
+      const int h = c / s.dh, d = c - h * s.dh;
+      const bool pair = (nl + 1 < p.N) && (d + 1 < s.dh);
+      if (b == 1) {  // temporal branch: plain [row][3D]
+        __nv_bfloat16* o = s.tm + m * 3 * D + which * D + c;
+        if (pair) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
+        else { o[0] = __float2bfloat16_rn(v[j]); if (nl + 1 < p.N) o[1] = __float2bfloat16_rn(v[j + 1]); }
+        continue;
+      }
+      const BranchOut& bo = b == 0 ? s.sp : s.fs;
+      // row -> (sequence, token) and key index
+      int64_t seq, tok, qrow, krow;
+      if (s.text_rows) {  // rows are prompt rows: keys [0, Lt) of the fs sequence
+        seq = 0; tok = m; qrow = -1; krow = m;
+      } else if (b == 0) {
+        seq = m / s.Lv; tok = m % s.Lv; qrow = m; krow = m;
+      } else {
+        seq = 0; tok = m + s.Lt; qrow = m; krow = m + s.Lt;
+      }
+      if (which == 0) {
+        if (qrow < 0) continue;
+        __nv_bfloat16* o = bo.q + (qrow * s.H + h) * s.DP + d;
+        if (pair) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
+        else { o[0] = __float2bfloat16_rn(v[j]); }
+        if (!pair && nl + 1 < p.N) {  // pair straddles a head boundary
+          const int c1 = c + 1, h1 = c1 / s.dh, d1 = c1 - h1 * s.dh;
+          bo.q[(qrow * s.H + h1) * s.DP + d1] = __float2bfloat16_rn(v[j + 1]);
+        }
+      } else if (which == 1) {
+        __nv_bfloat16* o = bo.k + (krow * s.H + h) * s.DP + d;
+        if (pair) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
+        else { o[0] = __float2bfloat16_rn(v[j]); }
+        if (!pair && nl + 1 < p.N) {
+          const int c1 = c + 1, h1 = c1 / s.dh, d1 = c1 - h1 * s.dh;
+          bo.k[(krow * s.H + h1) * s.DP + d1] = __float2bfloat16_rn(v[j + 1]);
+        }
+      } else {
+        __nv_bfloat16* o = bo.vt + ((seq * s.H + h) * s.DP + d) * bo.ld_key + tok;
+        o[0] = __float2bfloat16_rn(v[j]);
+        if (nl + 1 < p.N) {
+          const int c1 = c + 1, h1 = c1 / s.dh, d1 = c1 - h1 * s.dh;
+          bo.vt[((seq * s.H + h1) * s.DP + d1) * bo.ld_key + tok] = __float2bfloat16_rn(v[j + 1]);
+        }
+      }
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmTcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr uint32_t kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * kBBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int num_m = (int)cdiv(p.M, BM), num_n = (int)cdiv(p.N, BN);
+  const int tiles = num_m * num_n;
+  const int kblocks = (int)cdiv(p.K, BK);
+
+  if (warp == 0 && ptx::elect_one()) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 128); }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::fence_before_sync();
+  __syncthreads();
+  ptx::fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      int s = 0; uint32_t ph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int mt = t % num_m, nt = t / num_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], kABytes + kBBytes);
+          ptx::tma_load_2d(sA + s * kABytes, &tmA, &full[s], kb * BK, mt * BM);
+          ptx::tma_load_2d(sB + s * kBBytes, &tmB, &full[s], kb * BK, nt * BN);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
+    int s = 0; uint32_t ph = 0; int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+      ptx::fence_after_sync();
+      const uint32_t dtmem = tmem_base + acc * 256;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        ptx::mbar_wait(&full[s], ph);
+        ptx::fence_after_sync();
+        if (ptx::elect_one()) {
+          const uint32_t a0 = ptx::smem_u32(sA + s * kABytes);
+          const uint32_t b0 = ptx::smem_u32(sB + s * kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = ptx::smem_desc(a0 + kk * 32, 0, 1024, ptx::kLayoutSW128);
+            const uint64_t bd = ptx::smem_desc(b0 + kk * 32, 0, 1024, ptx::kLayoutSW128);
+            ptx::mma_bf16_ss(dtmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          ptx::mma_commit(&empty[s]);
+          if (kb == kblocks - 1) ptx::mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int lane = threadIdx.x & 31;
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int mt = t % num_m, nt = t / num_m;
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::fence_after_sync();
+      const int64_t m = (int64_t)mt * BM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int c = 0; c < BN / 16; ++c) {
+        const int n0 = nt * BN + c * 16;
+        if (n0 >= p.N) break;
+        uint32_t r[16];
+        ptx::tmem_ld16(tbase + c * 16, r);
+        ptx::tmem_ld_wait();
+        epilogue_chunk<EPI>(p, m, n0, r);
+      }
+      ptx::fence_before_sync();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+  }
+  ptx::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::fence_after_sync();
+    ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ---- host side -------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int EPI>
+int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p,
+                cudaStream_t st) {
+  static bool attr_set = false;
+  constexpr size_t smem = smem_bytes<BN>();
+  if (!attr_set) {
+    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const int64_t tiles = cdiv(p.M, BM) * cdiv(p.N, BN);
+  const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  gemm_tc_kernel<BN, EPI><<<grid, kThreads, smem, st>>>(ta, tb, p);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+}  // namespace
+
+int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                      uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                      CUtensorMapSwizzle swz) {
+  auto enc = get_encode();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable (driver too old?)"); return VC_ECUDA; }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_pitch_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(2d) failed: %d (inner %llu outer %llu pitch %llu)", (int)r,
+              (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_pitch_bytes);
+    return VC_ECUDA;
+  }
+  return VC_OK;
+}
+
+int make_tmap_4d_bf16(CUtensorMap* map, const void* base, const uint64_t dims_[4],
+                      const uint64_t strides_bytes[3], const uint32_t box_[4],
+                      CUtensorMapSwizzle swz) {
+  auto enc = get_encode();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return VC_ECUDA; }
+  cuuint64_t dims[4] = {dims_[0], dims_[1], dims_[2], dims_[3]};
+  cuuint64_t strides[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
+  cuuint32_t box[4] = {box_[0], box_[1], box_[2], box_[3]};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(4d) failed: %d", (int)r);
+    return VC_ECUDA;
+  }
+  return VC_OK;
+}
+
+int gemm_tc_pick_bn(int N) {
+  // smallest padding waste among the instantiated tile widths
+  const int cands[3] = {256, 176, 128};
+  int best = 256;
+  int64_t best_pad = INT64_MAX;
+  for (int bn : cands) {
+    const int64_t pad = cdiv(N, bn) * bn - N;
+    if (pad < best_pad) { best_pad = pad; best = bn; }
+  }
+  return best;
+}
+
+int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const GemmTcParams& p,
+                   int epi, cudaStream_t st) {
+  if (p.M <= 0 || p.N <= 0) return VC_OK;
+  if (p.K <= 0 || (lda * 2) % 16 || (ldb * 2) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) {
+    set_error("tcgen05 GEMM needs 16-byte aligned operands and row pitches (lda %lld ldb %lld)",
+              (long long)lda, (long long)ldb);
+    return VC_EINVAL;
+  }
+  const int bn = gemm_tc_pick_bn(p.N);
+  CUtensorMap ta, tb;
+  VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
+  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn, CU_TENSOR_MAP_SWIZZLE_128B));
+#define VC_GEMM_CASE(BNV)                                                  \
+  if (bn == BNV) {                                                         \
+    if (epi == EPI_F32) return launch_impl<BNV, EPI_F32>(ta, tb, p, st);   \
+    if (epi == EPI_BF16) return launch_impl<BNV, EPI_BF16>(ta, tb, p, st); \
+    return launch_impl<BNV, EPI_QKV>(ta, tb, p, st);                       \
+  }
+  VC_GEMM_CASE(256)
+  VC_GEMM_CASE(176)
+  VC_GEMM_CASE(128)
+#undef VC_GEMM_CASE
+  set_error("internal: no GEMM tile for N=%d", p.N);
+  return VC_ENOTSUP;
+}
+
+}  // namespace vc

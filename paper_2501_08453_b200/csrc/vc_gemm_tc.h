@@ -1,0 +1,51 @@
+// tcgen05 GEMM interface (vc_gemm_tc.cu).
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "vc_common.cuh"
+
+namespace vc {
+
+enum { EPI_F32 = 0, EPI_BF16 = 1, EPI_QKV = 2 };
+
+// Attention-layout destination of one branch (spatial or full-sequence).
+struct BranchOut {
+  __nv_bfloat16* q;   // [q rows][H][DP]
+  __nv_bfloat16* k;   // [k rows][H][DP]
+  __nv_bfloat16* vt;  // [seq][H][DP][ld_key]
+  int64_t ld_key;
+};
+
+struct QkvScatter {
+  int64_t D, Lv, Lt;
+  int32_t H, dh, DP;
+  int32_t n_base;     // column of this GEMM's n=0 in the 9D space
+  int32_t text_rows;  // rows are prompt rows (full-sequence keys 0..Lt-1)
+  BranchOut sp, fs;
+  __nv_bfloat16* tm;  // temporal branch, plain [row][3D]
+};
+
+struct GemmTcParams {
+  int64_t M;
+  int32_t N, K;
+  const float* bias;  // [N] (indexed by local n) or null
+  float* out_f32; const float* R; int64_t ldr;
+  __nv_bfloat16* out_bf16;
+  int64_t ldo;
+  QkvScatter qkv;
+};
+
+// C = A[M][K] . B[N][K]^T with the selected epilogue.  A/B bf16 K-major.
+int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const GemmTcParams& p,
+                   int epi, cudaStream_t st);
+
+int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                      uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                      CUtensorMapSwizzle swz);
+int make_tmap_4d_bf16(CUtensorMap* map, const void* base, const uint64_t dims[4],
+                      const uint64_t strides_bytes[3], const uint32_t box[4],
+                      CUtensorMapSwizzle swz);
+int num_sms();
+
+}  // namespace vc

@@ -1,0 +1,44 @@
+// Internal launcher declarations shared between the .cu files.
+#pragma once
+#include "vc_common.cuh"
+
+namespace vc {
+
+struct GemmF32Args {
+  const float* A; int64_t lda;
+  const float* B; int64_t ldb;
+  const float* bias;
+  const float* R; int64_t ldr;
+  float* out; int64_t ldo;
+  int64_t M; int32_t N, K;
+};
+int launch_gemm_f32(const GemmF32Args& g, cudaStream_t st);
+
+template <typename T, typename OutT>
+int launch_attn_simt(const AttnArgs<T, OutT>& a, cudaStream_t st);
+
+template <typename OutT>
+int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
+                   cudaStream_t st);
+
+int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int h, int w,
+                 int c, int p, int D, double t, cudaStream_t st);
+int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h, int w, int c,
+                   int p, int D, cudaStream_t st);
+int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, bool bf16,
+                cudaStream_t st);
+
+// stage profiler (vc_profile.cu)
+bool profile_on();
+void profile_begin(cudaStream_t st);
+void profile_mark(cudaStream_t st, const char* name);
+void profile_end();
+
+// bf16 tensor-core path (vc_block_bf16.cu)
+size_t bf16_workspace_bytes(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H);
+int bf16_launch_count(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H);
+int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, const void* wqkv,
+                       const float* bias, const void* wo, const float* x, const float* prompt,
+                       float* out, int add_residual, char* ws, cudaStream_t st);
+
+}  // namespace vc

@@ -1,0 +1,240 @@
+// Memory-bound row kernels: LayerNorm row statistics, patch embed /
+// unembed, and the one-time weight pack.  Judged against HBM bandwidth.
+#include "vc_kernels.h"
+
+namespace vc {
+
+// ---------------------------------------------------------------------------
+// LayerNorm without affine, model.py:89-92: (x - mean) / sqrt(var + 1e-5),
+// biased variance.  The per-branch affine (gamma, beta) is folded into the
+// projection weights / bias at pack time, so one normalised copy of the rows
+// feeds all three branches' Q/K/V projections.  Rows come from two sources:
+// the visual tokens then the (anchored, deduplicated) prompt rows.
+// One warp per row; the row is held in registers between the passes.
+// ---------------------------------------------------------------------------
+template <typename OutT, int VPL>
+__global__ void __launch_bounds__(256) ln_rows_kernel(const float* __restrict__ x, int64_t n_x,
+                                                      const float* __restrict__ p, int64_t n_p,
+                                                      int D, OutT* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n_x + n_p) return;
+  const float* src = row < n_x ? x + row * D : p + (row - n_x) * D;
+  float v[VPL];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    int d = lane + 32 * i;
+    v[i] = d < D ? src[d] : 0.f;
+    s += v[i];
+  }
+  const float mean = warp_sum(s) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    int d = lane + 32 * i;
+    float c = d < D ? v[i] - mean : 0.f;
+    q = fmaf(c, c, q);
+  }
+  const float rstd = rsqrtf(warp_sum(q) / D + 1e-5f);
+  OutT* dst = out + row * D;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    int d = lane + 32 * i;
+    if (d < D) dst[d] = from_f32<OutT>((v[i] - mean) * rstd);
+  }
+}
+
+template <typename OutT>
+int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
+                   cudaStream_t st) {
+  int64_t rows = n_x + n_p;
+  if (rows <= 0) return VC_OK;
+  dim3 grid((unsigned)cdiv(rows, 8));
+  int vpl = (int)cdiv(D, 32);
+  if (vpl <= 4) ln_rows_kernel<OutT, 4><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out);
+  else if (vpl <= 16) ln_rows_kernel<OutT, 16><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out);
+  else if (vpl <= 50) ln_rows_kernel<OutT, 50><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out);
+  else if (vpl <= 96) ln_rows_kernel<OutT, 96><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out);
+  else {
+    set_error("LayerNorm supports dim <= 3072, got %d", D);
+    return VC_ENOTSUP;
+  }
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+template int launch_ln_rows<float>(const float*, int64_t, const float*, int64_t, int, float*, cudaStream_t);
+template int launch_ln_rows<__nv_bfloat16>(const float*, int64_t, const float*, int64_t, int, __nv_bfloat16*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// Patch embed, model.py:303-314 with patchify model.py:53-64 and
+// sinusoidal_embedding model.py:79-86.  x[f][i][d] = patch(f,i) . w_in[:,d]
+// + sinus(f*Lv + i)[d] + sinus(t)[d].  Angles and sin/cos in fp64 (the
+// global token index reaches 1e5-1e6 where an fp32 angle would be off by
+// 1e-2), the patch dot in fp64, stored fp32 (the residual stream).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double sinus(double pos, int d, int D) {
+  const int half = D >> 1;
+  const int k = d < half ? d : d - half;
+  const double freq = exp(-9.210340371976184 * (double)k / (double)half);  // -ln(1e4)
+  const double ang = pos * freq;
+  return d < half ? sin(ang) : cos(ang);
+}
+
+__global__ void embed_kernel(const float* __restrict__ lat, const float* __restrict__ w_in,
+                             float* __restrict__ x, int F, int first_frame, int h, int w, int c,
+                             int p, int D, double t) {
+  const int gh = (h + p - 1) / p, gw = (w + p - 1) / p;
+  const int Lv = gh * gw, pd = p * p * c;
+  const int64_t total = (int64_t)F * Lv * D;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)(e % D);
+    const int64_t tok = e / D;  // f*Lv + i
+    const int f = (int)(tok / Lv), i = (int)(tok % Lv);
+    const int gy = i / gw, gx = i % gw;
+    double acc = 0.0;
+    for (int j = 0; j < pd; ++j) {
+      const int py = j / (p * c), px = (j / c) % p, ch = j % c;
+      const int yy = gy * p + py, xx = gx * p + px;
+      if (yy < h && xx < w)
+        acc += (double)lat[(((int64_t)f * h + yy) * w + xx) * c + ch] * (double)w_in[(int64_t)j * D + d];
+    }
+    acc += sinus((double)(tok + (int64_t)first_frame * Lv), d, D);
+    acc += sinus(t, d, D);
+    x[e] = (float)acc;
+  }
+}
+
+// Unembed, model.py:331-333 + unpatchify model.py:67-76: one warp per token
+// computes its p*p*c outputs (x_tok . w_out) and scatters the in-bounds
+// pixels (the crop).
+template <int PD>
+__global__ void unembed_kernel(const float* __restrict__ x, const float* __restrict__ w_out,
+                               float* __restrict__ eps, int F, int h, int w, int c, int p, int D) {
+  const int gh = (h + p - 1) / p, gw = (w + p - 1) / p;
+  const int Lv = gh * gw, pd = p * p * c;
+  const int lane = threadIdx.x & 31;
+  const int64_t tok = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (tok >= (int64_t)F * Lv) return;
+  float acc[PD];
+#pragma unroll
+  for (int j = 0; j < PD; ++j) acc[j] = 0.f;
+  const float* xr = x + tok * D;
+  for (int d = lane; d < D; d += 32) {
+    const float xv = xr[d];
+#pragma unroll
+    for (int j = 0; j < PD; ++j)
+      if (j < pd) acc[j] = fmaf(xv, w_out[(int64_t)d * pd + j], acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < PD; ++j) acc[j] = warp_sum(acc[j]);
+  const int f = (int)(tok / Lv), i = (int)(tok % Lv);
+  const int gy = i / gw, gx = i % gw;
+#pragma unroll
+  for (int j = 0; j < PD; ++j) {
+    if (j >= pd || lane != (j & 31)) continue;
+    const int py = j / (p * c), px = (j / c) % p, ch = j % c;
+    const int yy = gy * p + py, xx = gx * p + px;
+    if (yy < h && xx < w) eps[(((int64_t)f * h + yy) * w + xx) * c + ch] = acc[j];
+  }
+}
+
+int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int h, int w,
+                 int c, int p, int D, double t, cudaStream_t st) {
+  const int64_t total = (int64_t)F * ((h + p - 1) / p) * ((w + p - 1) / p) * D;
+  if (total <= 0) return VC_OK;
+  const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+  embed_kernel<<<blocks, 256, 0, st>>>(lat, w_in, x, F, first_frame, h, w, c, p, D, t);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
+int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h, int w, int c,
+                   int p, int D, cudaStream_t st) {
+  const int64_t toks = (int64_t)F * ((h + p - 1) / p) * ((w + p - 1) / p);
+  const int pd = p * p * c;
+  if (toks <= 0) return VC_OK;
+  dim3 grid((unsigned)cdiv(toks, 8));
+  if (pd <= 16) unembed_kernel<16><<<grid, 256, 0, st>>>(x, w_out, eps, F, h, w, c, p, D);
+  else if (pd <= 64) unembed_kernel<64><<<grid, 256, 0, st>>>(x, w_out, eps, F, h, w, c, p, D);
+  else {
+    set_error("unembed supports patch*patch*channels <= 64, got %d", pd);
+    return VC_ENOTSUP;
+  }
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Weight pack (one-time).  raw = 3 branches x {gamma[D], beta[D], wq, wk, wv,
+// wo [D][D] row-major}.  Folding: (xhat*gamma + beta) @ W
+//   = xhat @ (diag(gamma) W) + beta @ W.
+// fp32 layout : Wqkv [D][9D] (x @ W orientation), bias [9D], Wo [3D][D]
+// bf16 layout : Wqkv^T [9D][D] (K-major for tcgen05), bias [9D] fp32,
+//               Wo^T [D][3D]
+// Column n of the 9D space = branch*3D + {q,k,v}*D + c.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ const float* raw_branch(const float* raw, int b, int D) {
+  return raw + (int64_t)b * (2 * (int64_t)D + 4 * (int64_t)D * D);
+}
+__device__ __forceinline__ const float* raw_w(const float* raw, int b, int which, int D) {
+  return raw_branch(raw, b, D) + 2 * (int64_t)D + (int64_t)which * D * D;  // which: 0 q,1 k,2 v,3 o
+}
+
+template <typename T, bool KMAJOR>
+__global__ void pack_qkv_kernel(const float* __restrict__ raw, T* __restrict__ wqkv, int D) {
+  // one thread per (k, n) of the 9D x D matrix
+  const int64_t total = (int64_t)9 * D * D;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n, k;
+    if (KMAJOR) { n = e / D; k = e % D; }      // output [9D][D], k fastest
+    else { k = e / (9 * (int64_t)D); n = e % (9 * (int64_t)D); }  // output [D][9D]
+    const int b = (int)(n / (3 * D)), which = (int)((n / D) % 3), c = (int)(n % D);
+    const float g = raw_branch(raw, b, D)[k];
+    const float wv = raw_w(raw, b, which, D)[k * D + c];
+    wqkv[e] = from_f32<T>(g * wv);
+  }
+}
+
+__global__ void pack_bias_kernel(const float* __restrict__ raw, float* __restrict__ bias, int D) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= 9 * D) return;
+  const int b = n / (3 * D), which = (n / D) % 3, c = n % D;
+  const float* beta = raw_branch(raw, b, D) + D;
+  const float* W = raw_w(raw, b, which, D);
+  double acc = 0.0;
+  for (int k = 0; k < D; ++k) acc += (double)beta[k] * (double)W[(int64_t)k * D + c];
+  bias[n] = (float)acc;
+}
+
+template <typename T, bool KMAJOR>
+__global__ void pack_o_kernel(const float* __restrict__ raw, T* __restrict__ wo, int D) {
+  const int64_t total = (int64_t)3 * D * D;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t kk, n;  // kk in [0, 3D): branch*D + k
+    if (KMAJOR) { n = e / (3 * (int64_t)D); kk = e % (3 * (int64_t)D); }  // [D][3D]
+    else { kk = e / D; n = e % D; }                                      // [3D][D]
+    const int b = (int)(kk / D), k = (int)(kk % D);
+    wo[e] = from_f32<T>(raw_w(raw, b, 3, D)[(int64_t)k * D + n]);
+  }
+}
+
+int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, bool bf16,
+                cudaStream_t st) {
+  const int blocks = 148 * 8;
+  if (bf16) {
+    pack_qkv_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wqkv, D);
+    pack_o_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wo, D);
+  } else {
+    pack_qkv_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wqkv, D);
+    pack_o_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wo, D);
+  }
+  pack_bias_kernel<<<(unsigned)cdiv(9 * D, 128), 128, 0, st>>>(raw, bias, D);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
+}  // namespace vc
