@@ -149,14 +149,22 @@ def cpu_sample(cfg_id, sample_frames):
     t1 = time.perf_counter()
     O.temporal_branch(blk.temporal, x, H)
     t2 = time.perf_counter()
-    O.full_sequence_attention(blk.fullseq, text, x, H)
+    # full-sequence branch (model.py:247-260) timed in its linear part
+    # (LN + Q/K/V projections of all S rows, O projection) and its S^2 part
+    p = blk.fullseq
+    seq = O.interleave_checkerboard(text, x)
+    q, k, v = O.branch_qkv(p, seq)
     t3 = time.perf_counter()
-    sp, tm, fs = t1 - t0, t2 - t1, t3 - t2
-    scale_f = F / Fs
-    s_ratio = (F * (Lt + Lv)) / (Fs * (Lt + Lv))
-    full = sp * scale_f + tm * scale_f + fs * s_ratio ** 2
-    return {"sample_s": t3 - t0, "full_s": full, "tokens": F * Lv,
-            "value": F * Lv / full, "branches_s": [sp, tm, fs], "Fs": Fs}
+    att = O.attention(q, k, v, H)
+    t4 = time.perf_counter()
+    O.deinterleave_visual(att @ p.wo, Fs, Lt, Lv)
+    t5 = time.perf_counter()
+    sp, tm = t1 - t0, t2 - t1
+    fs_lin, fs_quad = (t3 - t2) + (t5 - t4), t4 - t3
+    r = F / Fs
+    full = (sp + tm + fs_lin) * r + fs_quad * r * r
+    return {"sample_s": t5 - t0, "full_s": full, "tokens": F * Lv,
+            "value": F * Lv / full, "branches_s": [sp, tm, fs_lin, fs_quad], "Fs": Fs}
 
 
 def cpu_cores():
@@ -183,7 +191,7 @@ def run_reference_arm(args):
     full_s = float(np.median([r["full_s"] for r in samples]))
     sample = (f"oracle port (fp64 numpy, pinned to the reference's golden outputs) block forward of a "
               f"{samples[0]['Fs']}-frame clip of {name}, branches timed and extrapolated to F={F} "
-              f"(spatial,temporal ~F; full-sequence ~S^2); median of {args.steps} steps")
+              f"(spatial, temporal, full-seq projections ~F; full-seq attention ~F^2); median of {args.steps} steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -311,7 +319,7 @@ def run_gpu_arm(args):
         cpu = {"value": r["value"], "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
                "sample": (f"oracle port (fp64 numpy, pinned to reference golden outputs), {r['Fs']}-frame clip "
                           f"of the same geometry ({r['sample_s']:.1f} s), branches extrapolated to F={F} "
-                          f"(spatial,temporal ~F; full-seq ~S^2)")}
+                          f"(spatial, temporal, full-seq projections ~F; full-seq attention ~F^2)")}
 
     launches = lib.vc_block_forward_launches(C.byref(shp)) * args.steps
     line = {

@@ -69,15 +69,15 @@ def attention(q, k, v, heads: int, key_weight=None) -> np.ndarray:
         raise ValueError(f"feature dim {q.shape[-1]} not divisible by {heads} heads")
     d = q.shape[-1]
     dh = d // heads
-    qh = q.reshape(q.shape[:-1] + (heads, dh))
-    kh = k.reshape(k.shape[:-1] + (heads, dh))
-    vh = v.reshape(v.shape[:-1] + (heads, dh))
-    s = np.einsum("...qhd,...khd->...hqk", qh, kh) * (1.0 / np.sqrt(dh))
+    # [..., s, h, dh] -> [..., h, s, dh]; batched BLAS matmuls per head
+    qh = np.ascontiguousarray(np.swapaxes(q.reshape(q.shape[:-1] + (heads, dh)), -2, -3))
+    kh = np.ascontiguousarray(np.swapaxes(k.reshape(k.shape[:-1] + (heads, dh)), -2, -3))
+    vh = np.ascontiguousarray(np.swapaxes(v.reshape(v.shape[:-1] + (heads, dh)), -2, -3))
+    s = (qh @ np.swapaxes(kh, -1, -2)) * (1.0 / np.sqrt(dh))
     if key_weight is not None:
         s = s + np.log(key_weight)
-    p = softmax_rows(s)
-    o = np.einsum("...hqk,...khd->...qhd", p, vh)
-    return o.reshape(q.shape)
+    o = softmax_rows(s) @ vh
+    return np.ascontiguousarray(np.swapaxes(o, -2, -3)).reshape(q.shape)
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,367 @@
+// Flash attention on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Semantics: numerics.py:87-107 per (sequence, head), non-causal, applied to
+// the spatial branch (one sequence per frame, model.py:230-235) and the
+// anchored full sequence (model.py:247-260) with its F identical text copies
+// collapsed into ONE key segment whose logits carry + log2(F) (exact: a key
+// repeated F times has F times the softmax weight; reference key/value
+// permutation invariance, tests/test_numerics.py:131-140).
+//
+// Layouts (written by the QKV GEMM epilogue, vc_gemm_tc.cu EPI_QKV):
+//   Q  [seq][Lq][H][DP]  bf16, head dim zero-padded dh -> DP (64/80/128)
+//   K  [seq][Lk][H][DP]  (full sequence: keys 0..Lt-1 are the text keys)
+//   Vt [seq][H][DP][Lk_ld] V transposed: the K-major B operand of P.V
+// DP = 64*n64 (+16): the 64-wide part is TMA'd with 128B swizzle, a 16-wide
+// tail with 32B swizzle; each tcgen05.mma (K = 16) picks its descriptor.
+//
+// One CTA = 128 queries of one (sequence, head); 256 threads:
+//   w0 TMA producer (Q once, then K/Vt tiles of 128 keys, 2-stage ring)
+//   w1 MMA issuer: S(j+1) = Q K^T issued ahead of O += P(j) V(j)
+//   w2 TMEM owner (512 columns: S double buffer 2x128, O at 256)
+//   w4..w7 softmax: thread = query row = TMEM lane; online softmax in the
+//         log2 domain with lazy rescale (O in TMEM is rescaled only when the
+//         running max grows by > 8, so P <= 2^8), P -> bf16 -> smem (SW128
+//         K-major, double buffered) for the SS MMA.
+#include <math.h>
+
+#include "vc_attn_tc.h"
+#include "vc_gemm_tc.h"
+#include "vc_ptx.cuh"
+
+namespace vc {
+
+namespace {
+
+constexpr int BQ = 128, BKV = 128;
+constexpr int kThreads = 256;
+constexpr float kRescaleThreshold = 8.0f;
+
+template <int DP>
+struct Cfg {
+  static constexpr int N64 = DP / 64;                  // SW128 64-wide chunks of the head dim
+  static constexpr int TAIL = DP % 64;                 // 0 or 16 (SW32 chunk)
+  static_assert(TAIL == 0 || TAIL == 16, "DP must be 64*n or 64*n+16");
+  static constexpr int QK_BYTES = BQ * DP * 2;         // one Q (or K) tile
+  static constexpr int V_BYTES = DP * BKV * 2;         // one Vt tile (2 chunks of 64 keys)
+  static constexpr int P_BYTES = BQ * BKV * 2;         // one P tile
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + QK_BYTES;       // 2 stages
+  static constexpr int OFF_V = OFF_K + 2 * QK_BYTES;   // 2 stages
+  static constexpr int OFF_P = OFF_V + 2 * V_BYTES;    // 2 buffers
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int KSTEPS = DP / 16;               // MMA K steps of S = Q K^T
+};
+
+// Byte offset, inside a Q/K tile, of the head-dim 16-chunk c; tiles are laid
+// out as N64 SW128 sub-tiles [128 rows][128 B] followed by the SW32 tail
+// [128 rows][32 B].
+template <int DP>
+__device__ __forceinline__ uint64_t qk_desc(uint32_t tile_addr, int c) {
+  constexpr int N64 = Cfg<DP>::N64;
+  if (c < 4 * N64) {
+    const uint32_t a = tile_addr + (c >> 2) * (BQ * 128) + (c & 3) * 32;
+    return ptx::smem_desc(a, 0, 1024, ptx::kLayoutSW128);
+  }
+  return ptx::smem_desc(tile_addr + N64 * (BQ * 128), 0, 256, ptx::kLayoutSW32);
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
+                   const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
+                   const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
+  using CF = Cfg<DP>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_empty = bars + 7;   // [2]
+  uint64_t* p_full = bars + 9;    // [2]
+  uint64_t* pv_done = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x >> 5;
+  const int q0 = blockIdx.x * BQ;
+  const int h = blockIdx.y;
+  const int seq = blockIdx.z;
+  const int n_tiles = (p.Lk + BKV - 1) / BKV;
+
+  if (warp == 0 && ptx::elect_one()) {
+    ptx::prefetch_tmap(&tmQ64); ptx::prefetch_tmap(&tmK64); ptx::prefetch_tmap(&tmV);
+    if (CF::TAIL) { ptx::prefetch_tmap(&tmQ16); ptx::prefetch_tmap(&tmK16); }
+    ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&kv_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_empty[i], 128);
+      ptx::mbar_init(&p_full[i], 128);
+    }
+    ptx::mbar_init(pv_done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::fence_before_sync();
+  __syncthreads();
+  ptx::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem;          // S buffers at columns 0 and 128
+  const uint32_t tO = tmem + 256;    // O accumulator, DP columns
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (ptx::elect_one()) {
+      uint8_t* sQ = smem + CF::OFF_Q;
+      ptx::mbar_arrive_expect_tx(q_full, CF::QK_BYTES);
+      for (int c = 0; c < CF::N64; ++c)
+        ptx::tma_load_4d(sQ + c * BQ * 128, &tmQ64, q_full, c * 64, h, q0, seq);
+      if (CF::TAIL) ptx::tma_load_4d(sQ + CF::N64 * BQ * 128, &tmQ16, q_full, CF::N64 * 64, h, q0, seq);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j & 1;
+        ptx::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[s], CF::QK_BYTES + CF::V_BYTES);
+        uint8_t* sK = smem + CF::OFF_K + s * CF::QK_BYTES;
+        uint8_t* sV = smem + CF::OFF_V + s * CF::V_BYTES;
+        const int k0 = j * BKV;
+        for (int c = 0; c < CF::N64; ++c)
+          ptx::tma_load_4d(sK + c * BKV * 128, &tmK64, &kv_full[s], c * 64, h, k0, seq);
+        if (CF::TAIL) ptx::tma_load_4d(sK + CF::N64 * BKV * 128, &tmK16, &kv_full[s], CF::N64 * 64, h, k0, seq);
+        ptx::tma_load_4d(sV, &tmV, &kv_full[s], k0, 0, h, seq);
+        ptx::tma_load_4d(sV + DP * 128, &tmV, &kv_full[s], k0 + 64, 0, h, seq);
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKV);
+    constexpr uint32_t idO = ptx::idesc_bf16_f32(BQ, DP);
+    const uint32_t aQ = ptx::smem_u32(smem + CF::OFF_Q);
+    ptx::mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {
+      const int s = j & 1;
+      ptx::mbar_wait(&kv_full[s], (j >> 1) & 1);
+      ptx::mbar_wait(&s_empty[s], ((j >> 1) & 1) ^ 1);
+      ptx::fence_after_sync();
+      if (ptx::elect_one()) {
+        const uint32_t aK = ptx::smem_u32(smem + CF::OFF_K + s * CF::QK_BYTES);
+#pragma unroll
+        for (int c = 0; c < CF::KSTEPS; ++c)
+          ptx::mma_bf16_ss(tS + s * BKV, qk_desc<DP>(aQ, c), qk_desc<DP>(aK, c), idS, c > 0);
+        ptx::mma_commit(&s_full[s]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < n_tiles; ++j) {
+      if (j + 1 < n_tiles) issue_s(j + 1);
+      const int s = j & 1;
+      ptx::mbar_wait(&p_full[s], (j >> 1) & 1);
+      ptx::fence_after_sync();
+      if (ptx::elect_one()) {
+        const uint32_t aP = ptx::smem_u32(smem + CF::OFF_P + s * CF::P_BYTES);
+        const uint32_t aV = ptx::smem_u32(smem + CF::OFF_V + s * CF::V_BYTES);
+#pragma unroll
+        for (int c = 0; c < BKV / 16; ++c) {
+          const uint64_t ad = ptx::smem_desc(aP + (c >> 2) * (BQ * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
+          const uint64_t bd = ptx::smem_desc(aV + (c >> 2) * (DP * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
+          ptx::mma_bf16_ss(tO, ad, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
+        }
+        ptx::mma_commit(&kv_empty[s]);
+        ptx::mma_commit(pv_done);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ===================== softmax / correction / epilogue =====================
+    const int qw = warp & 3;
+    const int lane = threadIdx.x & 31;
+    const int row = qw * 32 + lane;                 // query row in the tile = TMEM lane
+    const uint32_t lane_off = (uint32_t)(qw * 32) << 16;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j & 1;
+      const int k0 = j * BKV;
+      ptx::mbar_wait(&s_full[s], (j >> 1) & 1);
+      ptx::fence_after_sync();
+      float v[BKV];
+      {
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < BKV / 32; ++c) {
+          ptx::tmem_ld32(tS + s * BKV + lane_off + c * 32, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);
+        }
+      }
+      ptx::fence_before_sync();
+      ptx::mbar_arrive(&s_empty[s]);
+      // logits in the log2 domain: s * log2(e)/sqrt(dh) (+ log2 F on text keys)
+      const bool tail = k0 + BKV > p.Lk;
+      const bool biased = k0 < p.n_bias;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < BKV; ++i) {
+        float t = v[i] * p.scale_log2;
+        if (biased && k0 + i < p.n_bias) t += p.bias_log2;
+        if (tail && k0 + i >= p.Lk) t = -INFINITY;
+        v[i] = t;
+        mx = fmaxf(mx, t);
+      }
+      float alpha = 1.f;
+      if (mx > m_used + kRescaleThreshold) {
+        alpha = exp2f(m_used - mx);  // 0 on the first tile
+        m_used = mx;
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < BKV; ++i) {
+        v[i] = exp2f(v[i] - m_used);
+        sum += v[i];
+      }
+      l = l * alpha + sum;
+      // O (in TMEM) holds P(j-1) V(j-1) only after that MMA completes; the P
+      // buffer s was last read by PV(j-2), also complete by then.
+      if (j > 0) {
+        ptx::mbar_wait(pv_done, (j - 1) & 1);
+        ptx::fence_after_sync();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < DP / 16; ++c) {
+            uint32_t r[16];
+            ptx::tmem_ld16(tO + lane_off + c * 16, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            ptx::tmem_st16(tO + lane_off + c * 16, r);
+          }
+          ptx::tmem_st_wait();
+        }
+      }
+      // P -> bf16 -> smem, SW128 K-major: chunk of 64 keys, row pitch 128 B,
+      // 16-byte unit u of row r stored at u ^ (r & 7).
+      uint8_t* sP = smem + CF::OFF_P + s * CF::P_BYTES;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint8_t* rowp = sP + c * (BQ * 128) + row * 128;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float* pv = v + c * 64 + u * 8;
+          uint4 w;
+          __nv_bfloat162 b0 = __floats2bfloat162_rn(pv[0], pv[1]);
+          __nv_bfloat162 b1 = __floats2bfloat162_rn(pv[2], pv[3]);
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(pv[4], pv[5]);
+          __nv_bfloat162 b3 = __floats2bfloat162_rn(pv[6], pv[7]);
+          w.x = *reinterpret_cast<uint32_t*>(&b0);
+          w.y = *reinterpret_cast<uint32_t*>(&b1);
+          w.z = *reinterpret_cast<uint32_t*>(&b2);
+          w.w = *reinterpret_cast<uint32_t*>(&b3);
+          *reinterpret_cast<uint4*>(rowp + ((u ^ (row & 7)) << 4)) = w;
+        }
+      }
+      ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+      ptx::fence_before_sync();
+      ptx::mbar_arrive(&p_full[s]);
+    }
+    // ---- epilogue: O / l -> bf16 -> out[row][col_off + h*dh + d], d < dh ----
+    ptx::mbar_wait(pv_done, (n_tiles - 1) & 1);
+    ptx::fence_after_sync();
+    const int qi = q0 + row;
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = qi < p.Lq ? p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off + (int64_t)h * p.dh : nullptr;
+#pragma unroll
+    for (int c = 0; c < DP / 16; ++c) {
+      uint32_t r[16];
+      ptx::tmem_ld16(tO + lane_off + c * 16, r);
+      ptx::tmem_ld_wait();
+      if (orow) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const int d = c * 16 + i;
+          if (d + 1 < p.dh) {
+            __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv);
+            if (((p.col_off + h * p.dh + d) & 1) == 0)
+              *reinterpret_cast<__nv_bfloat162*>(orow + d) = b;
+            else { orow[d] = b.x; orow[d + 1] = b.y; }
+          } else if (d < p.dh) {
+            orow[d] = __float2bfloat16_rn(__uint_as_float(r[i]) * inv);
+          }
+        }
+      }
+    }
+  }
+  ptx::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::fence_after_sync();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int DP>
+int launch_dp(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+              int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
+  using CF = Cfg<DP>;
+  CUtensorMap mq64, mq16, mk64, mk16, mv;
+  const uint64_t eb = 2;
+  {
+    const uint64_t dims[4] = {(uint64_t)DP, (uint64_t)p.H, (uint64_t)p.Lq, (uint64_t)nseq};
+    const uint64_t str[3] = {DP * eb, (uint64_t)p.H * DP * eb, (uint64_t)q_rows_per_seq * p.H * DP * eb};
+    const uint32_t box64[4] = {64, 1, BQ, 1}, box16[4] = {16, 1, BQ, 1};
+    VC_TRY(make_tmap_4d_bf16(&mq64, q, dims, str, box64, CU_TENSOR_MAP_SWIZZLE_128B));
+    if (CF::TAIL) VC_TRY(make_tmap_4d_bf16(&mq16, q, dims, str, box16, CU_TENSOR_MAP_SWIZZLE_32B));
+    else mq16 = mq64;
+  }
+  {
+    const uint64_t dims[4] = {(uint64_t)DP, (uint64_t)p.H, (uint64_t)p.Lk, (uint64_t)nseq};
+    const uint64_t str[3] = {DP * eb, (uint64_t)p.H * DP * eb, (uint64_t)k_rows_per_seq * p.H * DP * eb};
+    const uint32_t box64[4] = {64, 1, BKV, 1}, box16[4] = {16, 1, BKV, 1};
+    VC_TRY(make_tmap_4d_bf16(&mk64, k, dims, str, box64, CU_TENSOR_MAP_SWIZZLE_128B));
+    if (CF::TAIL) VC_TRY(make_tmap_4d_bf16(&mk16, k, dims, str, box16, CU_TENSOR_MAP_SWIZZLE_32B));
+    else mk16 = mk64;
+  }
+  {
+    const uint64_t dims[4] = {(uint64_t)p.Lk, (uint64_t)DP, (uint64_t)p.H, (uint64_t)nseq};
+    const uint64_t str[3] = {(uint64_t)ld_key * eb, (uint64_t)DP * ld_key * eb, (uint64_t)p.H * DP * ld_key * eb};
+    const uint32_t box[4] = {64, DP, 1, 1};
+    VC_TRY(make_tmap_4d_bf16(&mv, vt, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B));
+  }
+  static bool attr = false;
+  if (!attr) {
+    VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    attr = true;
+  }
+  dim3 grid((unsigned)cdiv(p.Lq, BQ), (unsigned)p.H, (unsigned)nseq);
+  attn_tc_kernel<DP><<<grid, kThreads, CF::SMEM, st>>>(mq64, mq16, mk64, mk16, mv, p);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
+}  // namespace
+
+int attn_tc_head_pad(int dh) {
+  if (dh <= 64) return 64;
+  if (dh <= 80) return 80;
+  if (dh <= 128) return 128;
+  return 0;
+}
+
+int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+                   int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, int DP,
+                   cudaStream_t st) {
+  if (p.Lq <= 0 || nseq <= 0) return VC_OK;
+  if (p.Lk <= 0) { set_error("attention needs at least one key"); return VC_EINVAL; }
+  if (nseq > 65535 || p.H > 65535) { set_error("attention grid too large"); return VC_ENOTSUP; }
+  switch (DP) {
+    case 64: return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 80: return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 128: return launch_dp<128>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+  }
+  set_error("tcgen05 attention: unsupported padded head dim %d", DP);
+  return VC_ENOTSUP;
+}
+
+}  // namespace vc

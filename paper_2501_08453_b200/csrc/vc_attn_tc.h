@@ -1,0 +1,27 @@
+// tcgen05 flash attention interface (vc_attn_tc.cu).
+#pragma once
+#include "vc_common.cuh"
+
+namespace vc {
+
+struct AttnTcParams {
+  int32_t Lq, Lk, H, dh;
+  int32_t n_bias;       // keys [0, n_bias) get + bias_log2 (deduplicated anchored text)
+  float bias_log2;      // log2(F)
+  float scale_log2;     // log2(e) / sqrt(dh)
+  __nv_bfloat16* out;   // [seq * out_seq_rows + q][ld_out], head h at col_off + h*dh
+  int64_t ld_out;
+  int64_t col_off;
+  int64_t out_seq_rows;
+};
+
+// Padded head dim the tensor-core kernel uses for dh (0: unsupported).
+int attn_tc_head_pad(int dh);
+
+// q: [nseq][q_rows_per_seq][H][DP], k: [nseq][k_rows_per_seq][H][DP],
+// vt: [nseq][H][DP][ld_key] (bf16).
+int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+                   int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, int DP,
+                   cudaStream_t st);
+
+}  // namespace vc

@@ -1,7 +1,16 @@
-// bf16 block forward: tcgen05 projection GEMMs around the attention cores.
-// See vc_block.cu for the step list; this file owns the bf16 workspace.
+// bf16 block forward on tensor cores (see vc_block.cu for the step list).
+//
+//   ln (visual + prompt rows) -> xhat bf16
+//   QKV GEMM (tcgen05, N = 9D) whose epilogue scatters into the attention
+//     layouts: spatial / full-seq Q,K [row][H][DP] and V^T [seq][H][DP][key],
+//     temporal plain [row][3D]
+//   text K/V GEMM: the Lt prompt rows against the full-seq K,V columns only
+//   attention: spatial + full sequence on tcgen05 (vc_attn_tc.cu), temporal
+//     (F-token sequences, HBM-bound) on the SIMT kernel
+//   O GEMM (tcgen05, K = 3D) with the residual fused in the epilogue.
 #include <math.h>
 
+#include "vc_attn_tc.h"
 #include "vc_gemm_tc.h"
 #include "vc_kernels.h"
 
@@ -11,61 +20,83 @@ namespace {
 inline size_t aup(size_t v) { return (v + 1023) / 1024 * 1024; }
 
 struct WsBf16 {
-  size_t xhat, qkv, acat, total;
+  int64_t DP, Lv_ld, Lk_ld;
+  size_t xhat, qsp, ksp, vtsp, tm, qfs, kfs, vtfs, acat, total;
 };
-WsBf16 ws_layout(int64_t F, int64_t Lv, int64_t Lt, int64_t D) {
-  const int64_t Nv = F * Lv, rows = Nv + Lt;
+WsBf16 ws_layout(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
+  const int64_t Nv = F * Lv, dh = D / H;
   WsBf16 w;
-  w.xhat = 0;
-  w.qkv = aup(w.xhat + (size_t)rows * D * 2);
-  w.acat = aup(w.qkv + (size_t)rows * 9 * D * 2);
-  w.total = aup(w.acat + (size_t)Nv * 3 * D * 2);
+  w.DP = attn_tc_head_pad((int)dh);
+  w.Lv_ld = round_up(Lv, 8);
+  w.Lk_ld = round_up(Lt + Nv, 8);
+  const size_t qk = (size_t)H * w.DP * 2;
+  size_t o = 0;
+  w.xhat = o; o = aup(o + (size_t)(Nv + Lt) * D * 2);
+  w.qsp = o; o = aup(o + (size_t)Nv * qk);
+  w.ksp = o; o = aup(o + (size_t)Nv * qk);
+  w.vtsp = o; o = aup(o + (size_t)F * H * w.DP * w.Lv_ld * 2);
+  w.tm = o; o = aup(o + (size_t)Nv * 3 * D * 2);
+  w.qfs = o; o = aup(o + (size_t)Nv * qk);
+  w.kfs = o; o = aup(o + (size_t)(Lt + Nv) * qk);
+  w.vtfs = o; o = aup(o + (size_t)H * w.DP * w.Lk_ld * 2);
+  w.acat = o; o = aup(o + (size_t)Nv * 3 * D * 2);
+  w.total = o;
   return w;
 }
 }  // namespace
 
 size_t bf16_workspace_bytes(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
-  (void)H;
-  return ws_layout(F, Lv, Lt, D).total;
+  return ws_layout(F, Lv, Lt, D, H).total;
 }
 
-int bf16_launch_count(int64_t, int64_t, int64_t, int64_t, int64_t) { return 6; }
+int bf16_launch_count(int64_t, int64_t, int64_t Lt, int64_t, int64_t) { return Lt > 0 ? 7 : 6; }
 
 int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, const void* wqkv,
                        const float* bias, const void* wo, const float* x, const float* prompt,
                        float* out, int add_residual, char* ws, cudaStream_t st) {
-  const WsBf16 wl = ws_layout(F, Lv, Lt, D);
-  const int64_t Nv = F * Lv, rows = Nv + Lt, dh = D / H;
-  __nv_bfloat16* xhat = (__nv_bfloat16*)(ws + wl.xhat);
-  __nv_bfloat16* qkv = (__nv_bfloat16*)(ws + wl.qkv);
-  __nv_bfloat16* acat = (__nv_bfloat16*)(ws + wl.acat);
+  const WsBf16 wl = ws_layout(F, Lv, Lt, D, H);
+  const int64_t Nv = F * Lv, dh = D / H;
+  if (wl.DP == 0) { set_error("head dim %lld unsupported on the tensor-core path", (long long)dh); return VC_ENOTSUP; }
+  typedef __nv_bfloat16 bf;
+  bf* xhat = (bf*)(ws + wl.xhat);
+  bf* acat = (bf*)(ws + wl.acat);
+  bf* tm = (bf*)(ws + wl.tm);
 
-  VC_TRY(launch_ln_rows<__nv_bfloat16>(x, Nv, prompt, Lt, (int)D, xhat, st));
+  VC_TRY(launch_ln_rows<bf>(x, Nv, prompt, Lt, (int)D, xhat, st));
   profile_mark(st, "ln");
+
+  QkvScatter sc{};
+  sc.D = D; sc.Lv = Lv; sc.Lt = Lt; sc.H = (int)H; sc.dh = (int)dh; sc.DP = (int)wl.DP;
+  sc.sp = BranchOut{(bf*)(ws + wl.qsp), (bf*)(ws + wl.ksp), (bf*)(ws + wl.vtsp), wl.Lv_ld};
+  sc.fs = BranchOut{(bf*)(ws + wl.qfs), (bf*)(ws + wl.kfs), (bf*)(ws + wl.vtfs), wl.Lk_ld};
+  sc.tm = tm;
   {
     GemmTcParams g{};
-    g.M = rows; g.N = (int)(9 * D); g.K = (int)D;
-    g.bias = bias; g.out_bf16 = qkv; g.ldo = 9 * D;
-    VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_BF16, st));
+    g.M = Nv; g.N = (int)(9 * D); g.K = (int)D; g.bias = bias;
+    g.qkv = sc; g.qkv.n_base = 0; g.qkv.text_rows = 0;
+    VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_QKV, st));
   }
   profile_mark(st, "qkv_gemm");
+  if (Lt > 0) {
+    GemmTcParams g{};
+    g.M = Lt; g.N = (int)(2 * D); g.K = (int)D; g.bias = bias + 7 * D;
+    g.qkv = sc; g.qkv.n_base = (int)(7 * D); g.qkv.text_rows = 1;
+    VC_TRY(launch_gemm_tc(xhat + Nv * D, D, (const bf*)wqkv + 7 * D * D, D, g, EPI_QKV, st));
+    profile_mark(st, "text_kv_gemm");
+  }
   const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)dh));
-  const int64_t ld = 9 * D;
-  typedef AttnArgs<__nv_bfloat16, __nv_bfloat16> A;
   {
-    A a{};
-    a.q = qkv + 0 * D; a.ldq = ld; a.q_seq_stride = Lv; a.q_tok_stride = 1;
-    a.k = qkv + 1 * D; a.v = qkv + 2 * D; a.ldk = ld; a.k_seq_stride = Lv; a.k_tok_stride = 1;
-    a.o = acat + 0 * D; a.ldo = 3 * D; a.o_seq_stride = Lv; a.o_tok_stride = 1;
-    a.n_seq = (int)F; a.len_q = (int)Lv; a.len_k = (int)Lv; a.heads = (int)H; a.dh = (int)dh;
-    a.scale_log2 = scale_log2;
-    VC_TRY(launch_attn_simt(a, st));
+    AttnTcParams a{};
+    a.Lq = (int)Lv; a.Lk = (int)Lv; a.H = (int)H; a.dh = (int)dh;
+    a.n_bias = 0; a.bias_log2 = 0.f; a.scale_log2 = scale_log2;
+    a.out = acat; a.ld_out = 3 * D; a.col_off = 0; a.out_seq_rows = Lv;
+    VC_TRY(launch_attn_tc(a, sc.sp.q, sc.sp.k, sc.sp.vt, (int)F, Lv, Lv, wl.Lv_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_spatial");
   {
-    A a{};
-    a.q = qkv + 3 * D; a.ldq = ld; a.q_seq_stride = 1; a.q_tok_stride = Lv;
-    a.k = qkv + 4 * D; a.v = qkv + 5 * D; a.ldk = ld; a.k_seq_stride = 1; a.k_tok_stride = Lv;
+    AttnArgs<bf, bf> a{};
+    a.q = tm + 0 * D; a.ldq = 3 * D; a.q_seq_stride = 1; a.q_tok_stride = Lv;
+    a.k = tm + 1 * D; a.v = tm + 2 * D; a.ldk = 3 * D; a.k_seq_stride = 1; a.k_tok_stride = Lv;
     a.o = acat + 1 * D; a.ldo = 3 * D; a.o_seq_stride = 1; a.o_tok_stride = Lv;
     a.n_seq = (int)Lv; a.len_q = (int)F; a.len_k = (int)F; a.heads = (int)H; a.dh = (int)dh;
     a.scale_log2 = scale_log2;
@@ -73,15 +104,11 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   }
   profile_mark(st, "attn_temporal");
   {
-    A a{};
-    a.q = qkv + 6 * D; a.ldq = ld; a.q_seq_stride = 0; a.q_tok_stride = 1;
-    a.k = qkv + 7 * D; a.v = qkv + 8 * D; a.ldk = ld; a.k_seq_stride = 0; a.k_tok_stride = 1;
-    a.ka = qkv + Nv * ld + 7 * D; a.va = qkv + Nv * ld + 8 * D; a.lda = ld; a.na = (int)Lt;
-    a.log2_weight_a = (float)log2((double)F);
-    a.o = acat + 2 * D; a.ldo = 3 * D; a.o_seq_stride = 0; a.o_tok_stride = 1;
-    a.n_seq = 1; a.len_q = (int)Nv; a.len_k = (int)Nv; a.heads = (int)H; a.dh = (int)dh;
-    a.scale_log2 = scale_log2;
-    VC_TRY(launch_attn_simt(a, st));
+    AttnTcParams a{};
+    a.Lq = (int)Nv; a.Lk = (int)(Lt + Nv); a.H = (int)H; a.dh = (int)dh;
+    a.n_bias = (int)Lt; a.bias_log2 = (float)log2((double)F); a.scale_log2 = scale_log2;
+    a.out = acat; a.ld_out = 3 * D; a.col_off = 2 * D; a.out_seq_rows = 0;
+    VC_TRY(launch_attn_tc(a, sc.fs.q, sc.fs.k, sc.fs.vt, 1, Nv, Lt + Nv, wl.Lk_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_fullseq");
   {

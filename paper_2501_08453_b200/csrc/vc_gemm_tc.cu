@@ -37,6 +37,54 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// ---- QKV scatter helpers (branch b: 0 spatial, 2 full sequence) ----
+// GEMM row m -> Q row / K row / (sequence, key) of the attention layouts.
+__device__ __forceinline__ int64_t qkv_qrow(const QkvScatter& s, int b, int64_t m) {
+  (void)b;
+  return s.text_rows ? -1 : m;  // prompt rows have no queries (text is context)
+}
+__device__ __forceinline__ int64_t qkv_krow(const QkvScatter& s, int b, int64_t m) {
+  if (s.text_rows) return m;                 // full-sequence keys [0, Lt)
+  return b == 0 ? m : m + s.Lt;              // spatial: same row; full seq: after the text keys
+}
+__device__ __forceinline__ void qkv_vt_pos(const QkvScatter& s, int b, int64_t m, int64_t& seq,
+                                           int64_t& key) {
+  if (s.text_rows) { seq = 0; key = m; }
+  else if (b == 0) { seq = m / s.Lv; key = m - seq * s.Lv; }
+  else { seq = 0; key = m + s.Lt; }
+}
+// zero head h's padding columns [dh, DP) (Q/K) or padding rows (Vt) for row m
+__device__ __forceinline__ void qkv_zero_pad(const QkvScatter& s, int b, int which, int64_t m, int h) {
+  const BranchOut& bo = b == 0 ? s.sp : s.fs;
+  const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
+  if (which < 2) {
+    const int64_t row = which == 0 ? qkv_qrow(s, b, m) : qkv_krow(s, b, m);
+    if (row < 0) return;
+    __nv_bfloat16* o = (which == 0 ? bo.q : bo.k) + (row * s.H + h) * s.DP;
+    for (int d = s.dh; d < s.DP; ++d) o[d] = z;
+  } else {
+    int64_t seq, key;
+    qkv_vt_pos(s, b, m, seq, key);
+    for (int d = s.dh; d < s.DP; ++d) bo.vt[((seq * s.H + h) * s.DP + d) * bo.ld_key + key] = z;
+  }
+}
+__device__ __forceinline__ void qkv_store1(const QkvScatter& s, int b, int which, int64_t m, int c,
+                                           float val) {
+  const BranchOut& bo = b == 0 ? s.sp : s.fs;
+  const int h = c / s.dh, d = c - h * s.dh;
+  const __nv_bfloat16 x = __float2bfloat16_rn(val);
+  if (which < 2) {
+    const int64_t row = which == 0 ? qkv_qrow(s, b, m) : qkv_krow(s, b, m);
+    if (row < 0) return;
+    (which == 0 ? bo.q : bo.k)[(row * s.H + h) * s.DP + d] = x;
+  } else {
+    int64_t seq, key;
+    qkv_vt_pos(s, b, m, seq, key);
+    bo.vt[((seq * s.H + h) * s.DP + d) * bo.ld_key + key] = x;
+  }
+  if (d == s.dh - 1) qkv_zero_pad(s, b, which, m, h);
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m, int n0,
                                                const uint32_t (&r)[16]) {
@@ -88,53 +136,30 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
     for (int j = 0; j < 16; j += 2) {
       const int nl = n0 + j;
       if (nl >= p.N) break;
-      const int64_t n = nl + s.n_base;  // column in the 9D space
+      const int64_t n = nl + s.n_base;  // column in the 9D space (even: D even, n0 % 16 == 0)
       const int b = (int)(n / (3 * D));
       const int which = (int)((n / D) % 3);
-      const int c = (int)(n % D);
-      const int h = c / s.dh, d = c - h * s.dh;
-      const bool pair = (nl + 1 < p.N) && (d + 1 < s.dh);
+      const int c = (int)(n % D);   // c and c+1 share (branch, which) since c is even
+      const bool has2 = nl + 1 < p.N;
       if (b == 1) {  // temporal branch: plain [row][3D]
         __nv_bfloat16* o = s.tm + m * 3 * D + which * D + c;
-        if (pair) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
-        else { o[0] = __float2bfloat16_rn(v[j]); if (nl + 1 < p.N) o[1] = __float2bfloat16_rn(v[j + 1]); }
+        if (has2) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
+        else o[0] = __float2bfloat16_rn(v[j]);
         continue;
       }
-      const BranchOut& bo = b == 0 ? s.sp : s.fs;
-      // row -> (sequence, token) and key index
-      int64_t seq, tok, qrow, krow;
-      if (s.text_rows) {  // rows are prompt rows: keys [0, Lt) of the fs sequence
-        seq = 0; tok = m; qrow = -1; krow = m;
-      } else if (b == 0) {
-        seq = m / s.Lv; tok = m % s.Lv; qrow = m; krow = m;
-      } else {
-        seq = 0; tok = m + s.Lt; qrow = m; krow = m + s.Lt;
+      const int h = c / s.dh, d = c - h * s.dh;
+      if (has2 && which < 2 && d + 1 < s.dh && (d & 1) == 0) {  // 4-byte pair store
+        const int64_t row = which == 0 ? qkv_qrow(s, b, m) : qkv_krow(s, b, m);
+        if (row >= 0) {
+          __nv_bfloat16* base = (which == 0 ? (b == 0 ? s.sp.q : s.fs.q) : (b == 0 ? s.sp.k : s.fs.k));
+          __nv_bfloat16* o = base + (row * s.H + h) * s.DP + d;
+          *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
+          if (d + 2 == s.dh) qkv_zero_pad(s, b, which, m, h);
+        }
+        continue;
       }
-      if (which == 0) {
-        if (qrow < 0) continue;
-        __nv_bfloat16* o = bo.q + (qrow * s.H + h) * s.DP + d;
-        if (pair) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
-        else { o[0] = __float2bfloat16_rn(v[j]); }
-        if (!pair && nl + 1 < p.N) {  // pair straddles a head boundary
-          const int c1 = c + 1, h1 = c1 / s.dh, d1 = c1 - h1 * s.dh;
-          bo.q[(qrow * s.H + h1) * s.DP + d1] = __float2bfloat16_rn(v[j + 1]);
-        }
-      } else if (which == 1) {
-        __nv_bfloat16* o = bo.k + (krow * s.H + h) * s.DP + d;
-        if (pair) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
-        else { o[0] = __float2bfloat16_rn(v[j]); }
-        if (!pair && nl + 1 < p.N) {
-          const int c1 = c + 1, h1 = c1 / s.dh, d1 = c1 - h1 * s.dh;
-          bo.k[(krow * s.H + h1) * s.DP + d1] = __float2bfloat16_rn(v[j + 1]);
-        }
-      } else {
-        __nv_bfloat16* o = bo.vt + ((seq * s.H + h) * s.DP + d) * bo.ld_key + tok;
-        o[0] = __float2bfloat16_rn(v[j]);
-        if (nl + 1 < p.N) {
-          const int c1 = c + 1, h1 = c1 / s.dh, d1 = c1 - h1 * s.dh;
-          bo.vt[((seq * s.H + h1) * s.DP + d1) * bo.ld_key + tok] = __float2bfloat16_rn(v[j + 1]);
-        }
-      }
+      qkv_store1(s, b, which, m, c, v[j]);
+      if (has2) qkv_store1(s, b, which, m, c + 1, v[j + 1]);
     }
   }
 }
