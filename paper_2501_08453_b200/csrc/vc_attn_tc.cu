@@ -188,40 +188,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::fence_after_sync();
       float v[BKV];
       {
-        uint32_t r[32];
+        uint32_t r[BKV];
 #pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) {
-          ptx::tmem_ld32(tS + s * BKV + lane_off + c * 32, r);
-          ptx::tmem_ld_wait();
+        for (int c = 0; c < BKV / 32; ++c)
+          ptx::tmem_ld32(tS + s * BKV + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+        ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);
-        }
+        for (int i = 0; i < BKV; ++i) v[i] = __uint_as_float(r[i]);
       }
       ptx::fence_before_sync();
       ptx::mbar_arrive(&s_empty[s]);
-      // logits in the log2 domain: s * log2(e)/sqrt(dh) (+ log2 F on text keys)
-      const bool tail = k0 + BKV > p.Lk;
-      const bool biased = k0 < p.n_bias;
-      float mx = -INFINITY;
+      // logits in the log2 domain: s * log2(e)/sqrt(dh) (+ log2 F on text keys).
+      // Interior tiles keep raw scores and fold the scale into one FFMA below;
+      // text-key and tail tiles (warp-uniform) are converted explicitly.
+      float scale = p.scale_log2;
+      if (k0 < p.n_bias || k0 + BKV > p.Lk) {
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) {
-        float t = v[i] * p.scale_log2;
-        if (biased && k0 + i < p.n_bias) t += p.bias_log2;
-        if (tail && k0 + i >= p.Lk) t = -INFINITY;
-        v[i] = t;
-        mx = fmaxf(mx, t);
+        for (int i = 0; i < BKV; ++i) {
+          float t = v[i] * p.scale_log2;
+          if (k0 + i < p.n_bias) t += p.bias_log2;
+          if (k0 + i >= p.Lk) t = -INFINITY;
+          v[i] = t;
+        }
+        scale = 1.f;
+      }
+      float mx;
+      {
+        float m8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m8[i] = v[i];
+#pragma unroll
+        for (int i = 8; i < BKV; ++i) m8[i & 7] = fmaxf(m8[i & 7], v[i]);
+        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale;
       }
       float alpha = 1.f;
       if (mx > m_used + kRescaleThreshold) {
-        alpha = exp2f(m_used - mx);  // 0 on the first tile
+        alpha = ptx::ex2(m_used - mx);  // 0 on the first tile
         m_used = mx;
       }
-      float sum = 0.f;
+      const float neg_m = -m_used;
+      float s8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s8[i] = 0.f;
 #pragma unroll
       for (int i = 0; i < BKV; ++i) {
-        v[i] = exp2f(v[i] - m_used);
-        sum += v[i];
+        v[i] = ptx::ex2(fmaf(v[i], scale, neg_m));
+        s8[i & 7] += v[i];
       }
+      const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
       l = l * alpha + sum;
       // O (in TMEM) holds P(j-1) V(j-1) only after that MMA completes; the P
       // buffer s was last read by PV(j-2), also complete by then.

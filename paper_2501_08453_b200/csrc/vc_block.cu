@@ -81,10 +81,12 @@ struct PackedLayout {
 };
 static PackedLayout packed_layout(const Dims& d) {
   const size_t es = d.bf16 ? 2 : 4;
+  // bf16: head-padded QKV column space (vc_kernels.h QkvPad); fp32: plain 9D
+  const int64_t nq = d.bf16 ? qkv_pad_layout(d.D, d.H).Npad : 9 * d.D;
   PackedLayout p;
   p.wqkv = 0;
-  p.bias = align_up(p.wqkv + (size_t)9 * d.D * d.D * es, 1024);
-  p.wo = align_up(p.bias + (size_t)9 * d.D * 4, 1024);
+  p.bias = align_up(p.wqkv + (size_t)nq * d.D * es, 1024);
+  p.wo = align_up(p.bias + (size_t)nq * 4, 1024);
   p.total = align_up(p.wo + (size_t)3 * d.D * d.D * es, 1024);
   return p;
 }
@@ -223,8 +225,8 @@ int vc_pack_block_weights(const vc_block_shape* shape, const float* raw_dev, voi
   if (!raw_dev || !packed_dev) { set_error("null weight pointer"); return VC_EINVAL; }
   const PackedLayout pl = packed_layout(d);
   char* p = (char*)packed_dev;
-  return launch_pack(raw_dev, p + pl.wqkv, (float*)(p + pl.bias), p + pl.wo, (int)d.D, d.bf16,
-                     (cudaStream_t)stream);
+  return launch_pack(raw_dev, p + pl.wqkv, (float*)(p + pl.bias), p + pl.wo, (int)d.D, (int)d.H,
+                     d.bf16, (cudaStream_t)stream);
 }
 
 int vc_block_forward(const vc_block_shape* shape, const void* packed_dev, const float* visual_dev,

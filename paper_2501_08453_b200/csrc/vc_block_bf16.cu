@@ -26,7 +26,7 @@ struct WsBf16 {
 WsBf16 ws_layout(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
   const int64_t Nv = F * Lv, dh = D / H;
   WsBf16 w;
-  w.DP = attn_tc_head_pad((int)dh);
+  w.DP = qkv_head_pad(dh);
   w.Lv_ld = round_up(Lv, 8);
   w.Lk_ld = round_up(Lt + Nv, 8);
   const size_t qk = (size_t)H * w.DP * 2;
@@ -65,23 +65,25 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   VC_TRY(launch_ln_rows<bf>(x, Nv, prompt, Lt, (int)D, xhat, st));
   profile_mark(st, "ln");
 
+  const QkvPad pad = qkv_pad_layout(D, H);
   QkvScatter sc{};
-  sc.D = D; sc.Lv = Lv; sc.Lt = Lt; sc.H = (int)H; sc.dh = (int)dh; sc.DP = (int)wl.DP;
+  sc.pad = pad; sc.D = D; sc.Lv = Lv; sc.Lt = Lt; sc.H = (int)H;
   sc.sp = BranchOut{(bf*)(ws + wl.qsp), (bf*)(ws + wl.ksp), (bf*)(ws + wl.vtsp), wl.Lv_ld};
   sc.fs = BranchOut{(bf*)(ws + wl.qfs), (bf*)(ws + wl.kfs), (bf*)(ws + wl.vtfs), wl.Lk_ld};
   sc.tm = tm;
   {
     GemmTcParams g{};
-    g.M = Nv; g.N = (int)(9 * D); g.K = (int)D; g.bias = bias;
+    g.M = Nv; g.N = (int)pad.Npad; g.K = (int)D; g.bias = bias;
     g.qkv = sc; g.qkv.n_base = 0; g.qkv.text_rows = 0;
     VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_QKV, st));
   }
   profile_mark(st, "qkv_gemm");
-  if (Lt > 0) {
+  if (Lt > 0) {  // prompt rows: only the full-sequence K and V segments
+    const int64_t n0 = pad.fs_base() + pad.SEG;
     GemmTcParams g{};
-    g.M = Lt; g.N = (int)(2 * D); g.K = (int)D; g.bias = bias + 7 * D;
-    g.qkv = sc; g.qkv.n_base = (int)(7 * D); g.qkv.text_rows = 1;
-    VC_TRY(launch_gemm_tc(xhat + Nv * D, D, (const bf*)wqkv + 7 * D * D, D, g, EPI_QKV, st));
+    g.M = Lt; g.N = (int)(2 * pad.SEG); g.K = (int)D; g.bias = bias + n0;
+    g.qkv = sc; g.qkv.n_base = n0; g.qkv.text_rows = 1;
+    VC_TRY(launch_gemm_tc(xhat + Nv * D, D, (const bf*)wqkv + n0 * D, D, g, EPI_QKV, st));
     profile_mark(st, "text_kv_gemm");
   }
   const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)dh));

@@ -37,52 +37,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// ---- QKV scatter helpers (branch b: 0 spatial, 2 full sequence) ----
+// ---- QKV scatter (EPI_QKV) ----
 // GEMM row m -> Q row / K row / (sequence, key) of the attention layouts.
-__device__ __forceinline__ int64_t qkv_qrow(const QkvScatter& s, int b, int64_t m) {
-  (void)b;
-  return s.text_rows ? -1 : m;  // prompt rows have no queries (text is context)
-}
-__device__ __forceinline__ int64_t qkv_krow(const QkvScatter& s, int b, int64_t m) {
-  if (s.text_rows) return m;                 // full-sequence keys [0, Lt)
-  return b == 0 ? m : m + s.Lt;              // spatial: same row; full seq: after the text keys
-}
-__device__ __forceinline__ void qkv_vt_pos(const QkvScatter& s, int b, int64_t m, int64_t& seq,
-                                           int64_t& key) {
-  if (s.text_rows) { seq = 0; key = m; }
-  else if (b == 0) { seq = m / s.Lv; key = m - seq * s.Lv; }
-  else { seq = 0; key = m + s.Lt; }
-}
-// zero head h's padding columns [dh, DP) (Q/K) or padding rows (Vt) for row m
-__device__ __forceinline__ void qkv_zero_pad(const QkvScatter& s, int b, int which, int64_t m, int h) {
-  const BranchOut& bo = b == 0 ? s.sp : s.fs;
-  const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
-  if (which < 2) {
-    const int64_t row = which == 0 ? qkv_qrow(s, b, m) : qkv_krow(s, b, m);
-    if (row < 0) return;
-    __nv_bfloat16* o = (which == 0 ? bo.q : bo.k) + (row * s.H + h) * s.DP;
-    for (int d = s.dh; d < s.DP; ++d) o[d] = z;
-  } else {
-    int64_t seq, key;
-    qkv_vt_pos(s, b, m, seq, key);
-    for (int d = s.dh; d < s.DP; ++d) bo.vt[((seq * s.H + h) * s.DP + d) * bo.ld_key + key] = z;
+__device__ __forceinline__ void qkv_rows(const QkvScatter& s, int b, int64_t m, int64_t& qrow,
+                                         int64_t& krow, int64_t& seq, int64_t& key) {
+  if (s.text_rows) {            // prompt rows: full-sequence keys [0, Lt), no queries
+    qrow = -1; krow = m; seq = 0; key = m;
+  } else if (b == 0) {          // spatial: one sequence per frame
+    qrow = m; krow = m; seq = m / s.Lv; key = m - seq * s.Lv;
+  } else {                      // full sequence: text keys first, then visual
+    qrow = m; krow = m + s.Lt; seq = 0; key = m + s.Lt;
   }
-}
-__device__ __forceinline__ void qkv_store1(const QkvScatter& s, int b, int which, int64_t m, int c,
-                                           float val) {
-  const BranchOut& bo = b == 0 ? s.sp : s.fs;
-  const int h = c / s.dh, d = c - h * s.dh;
-  const __nv_bfloat16 x = __float2bfloat16_rn(val);
-  if (which < 2) {
-    const int64_t row = which == 0 ? qkv_qrow(s, b, m) : qkv_krow(s, b, m);
-    if (row < 0) return;
-    (which == 0 ? bo.q : bo.k)[(row * s.H + h) * s.DP + d] = x;
-  } else {
-    int64_t seq, key;
-    qkv_vt_pos(s, b, m, seq, key);
-    bo.vt[((seq * s.H + h) * s.DP + d) * bo.ld_key + key] = x;
-  }
-  if (d == s.dh - 1) qkv_zero_pad(s, b, which, m, h);
 }
 
 template <int EPI>
@@ -129,37 +94,51 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
       for (int j = 0; j < 16; ++j)
         if (n0 + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
     }
-  } else {  // EPI_QKV
+  } else {  // EPI_QKV: 16 columns of the head-padded space (vc_kernels.h QkvPad)
     const QkvScatter& s = p.qkv;
-    const int64_t D = s.D;
+    const QkvPad& q = s.pad;
+    const int64_t n = n0 + s.n_base;
+    if (n >= 3 * q.SEG && n < q.fs_base()) {  // temporal: plain [row][3D]
+      const int64_t j = n - 3 * q.SEG;
+      __nv_bfloat16* o = s.tm + m * 3 * s.D + j;
+      if (j + 16 <= 3 * s.D && n0 + 16 <= p.N) {
+        uint4 a, b;
+        a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);
+        a.z = pack_bf16x2(v[4], v[5]); a.w = pack_bf16x2(v[6], v[7]);
+        b.x = pack_bf16x2(v[8], v[9]); b.y = pack_bf16x2(v[10], v[11]);
+        b.z = pack_bf16x2(v[12], v[13]); b.w = pack_bf16x2(v[14], v[15]);
+        reinterpret_cast<uint4*>(o)[0] = a;
+        reinterpret_cast<uint4*>(o)[1] = b;
+      } else {
 #pragma unroll
-    for (int j = 0; j < 16; j += 2) {
-      const int nl = n0 + j;
-      if (nl >= p.N) break;
-      const int64_t n = nl + s.n_base;  // column in the 9D space (even: D even, n0 % 16 == 0)
-      const int b = (int)(n / (3 * D));
-      const int which = (int)((n / D) % 3);
-      const int c = (int)(n % D);   // c and c+1 share (branch, which) since c is even
-      const bool has2 = nl + 1 < p.N;
-      if (b == 1) {  // temporal branch: plain [row][3D]
-        __nv_bfloat16* o = s.tm + m * 3 * D + which * D + c;
-        if (has2) *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
-        else o[0] = __float2bfloat16_rn(v[j]);
-        continue;
+        for (int i = 0; i < 16; ++i)
+          if (j + i < 3 * s.D && n0 + i < p.N) o[i] = __float2bfloat16_rn(v[i]);
       }
-      const int h = c / s.dh, d = c - h * s.dh;
-      if (has2 && which < 2 && d + 1 < s.dh && (d & 1) == 0) {  // 4-byte pair store
-        const int64_t row = which == 0 ? qkv_qrow(s, b, m) : qkv_krow(s, b, m);
-        if (row >= 0) {
-          __nv_bfloat16* base = (which == 0 ? (b == 0 ? s.sp.q : s.fs.q) : (b == 0 ? s.sp.k : s.fs.k));
-          __nv_bfloat16* o = base + (row * s.H + h) * s.DP + d;
-          *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v[j], v[j + 1]);
-          if (d + 2 == s.dh) qkv_zero_pad(s, b, which, m, h);
-        }
-        continue;
-      }
-      qkv_store1(s, b, which, m, c, v[j]);
-      if (has2) qkv_store1(s, b, which, m, c + 1, v[j + 1]);
+      return;
+    }
+    const int b = n < 3 * q.SEG ? 0 : 2;
+    const int64_t r = b == 0 ? n : n - q.fs_base();
+    const int which = (int)(r / q.SEG);
+    const int64_t jj = r - which * q.SEG;
+    const int h = (int)(jj / q.DP), d0 = (int)(jj % q.DP);  // 16 | DP: the chunk is inside head h
+    const BranchOut& bo = b == 0 ? s.sp : s.fs;
+    int64_t qrow, krow, seq, key;
+    qkv_rows(s, b, m, qrow, krow, seq, key);
+    if (which < 2) {
+      const int64_t row = which == 0 ? qrow : krow;
+      if (row < 0) return;
+      __nv_bfloat16* o = (which == 0 ? bo.q : bo.k) + (row * s.H + h) * q.DP + d0;
+      uint4 a, c;
+      a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);
+      a.z = pack_bf16x2(v[4], v[5]); a.w = pack_bf16x2(v[6], v[7]);
+      c.x = pack_bf16x2(v[8], v[9]); c.y = pack_bf16x2(v[10], v[11]);
+      c.z = pack_bf16x2(v[12], v[13]); c.w = pack_bf16x2(v[14], v[15]);
+      reinterpret_cast<uint4*>(o)[0] = a;
+      reinterpret_cast<uint4*>(o)[1] = c;
+    } else {  // V^T: 16 head dims of one key; lanes are consecutive keys (coalesced)
+      __nv_bfloat16* o = bo.vt + ((seq * s.H + h) * q.DP + d0) * bo.ld_key + key;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[(int64_t)i * bo.ld_key] = __float2bfloat16_rn(v[i]);
     }
   }
 }
@@ -354,7 +333,7 @@ int make_tmap_4d_bf16(CUtensorMap* map, const void* base, const uint64_t dims_[4
 
 int gemm_tc_pick_bn(int N) {
   // smallest padding waste among the instantiated tile widths
-  const int cands[3] = {256, 176, 128};
+  const int cands[4] = {256, 240, 176, 128};
   int best = 256;
   int64_t best_pad = INT64_MAX;
   for (int bn : cands) {
@@ -365,14 +344,14 @@ int gemm_tc_pick_bn(int N) {
 }
 
 int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const GemmTcParams& p,
-                   int epi, cudaStream_t st) {
+                   int epi, cudaStream_t st, int bn) {
   if (p.M <= 0 || p.N <= 0) return VC_OK;
   if (p.K <= 0 || (lda * 2) % 16 || (ldb * 2) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) {
     set_error("tcgen05 GEMM needs 16-byte aligned operands and row pitches (lda %lld ldb %lld)",
               (long long)lda, (long long)ldb);
     return VC_EINVAL;
   }
-  const int bn = gemm_tc_pick_bn(p.N);
+  if (bn == 0) bn = gemm_tc_pick_bn(p.N);
   CUtensorMap ta, tb;
   VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
   VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn, CU_TENSOR_MAP_SWIZZLE_128B));
@@ -383,10 +362,11 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     return launch_impl<BNV, EPI_QKV>(ta, tb, p, st);                       \
   }
   VC_GEMM_CASE(256)
+  VC_GEMM_CASE(240)
   VC_GEMM_CASE(176)
   VC_GEMM_CASE(128)
 #undef VC_GEMM_CASE
-  set_error("internal: no GEMM tile for N=%d", p.N);
+  set_error("internal: no GEMM tile of width %d", bn);
   return VC_ENOTSUP;
 }
 

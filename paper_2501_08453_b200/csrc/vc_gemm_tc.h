@@ -3,7 +3,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include "vc_common.cuh"
+#include "vc_kernels.h"
 
 namespace vc {
 
@@ -18,9 +18,10 @@ struct BranchOut {
 };
 
 struct QkvScatter {
+  QkvPad pad;         // head-padded column space (vc_kernels.h)
   int64_t D, Lv, Lt;
-  int32_t H, dh, DP;
-  int32_t n_base;     // column of this GEMM's n=0 in the 9D space
+  int32_t H;
+  int64_t n_base;     // column of this GEMM's n=0 in the padded space
   int32_t text_rows;  // rows are prompt rows (full-sequence keys 0..Lt-1)
   BranchOut sp, fs;
   __nv_bfloat16* tm;  // temporal branch, plain [row][3D]
@@ -37,8 +38,9 @@ struct GemmTcParams {
 };
 
 // C = A[M][K] . B[N][K]^T with the selected epilogue.  A/B bf16 K-major.
+// bn: N tile width (0 = pick the least padding among 256/240/176/128).
 int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const GemmTcParams& p,
-                   int epi, cudaStream_t st);
+                   int epi, cudaStream_t st, int bn = 0);
 
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                       uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,

@@ -25,7 +25,30 @@ int launch_embed(const float* lat, const float* w_in, float* x, int F, int first
                  int c, int p, int D, double t, cudaStream_t st);
 int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h, int w, int c,
                    int p, int D, cudaStream_t st);
-int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, bool bf16,
+// Column space of the bf16 QKV GEMM: the spatial / full-sequence Q, K, V
+// segments are head-padded (H heads x DP columns, dh real + DP-dh zero
+// weight columns) so every 16-column chunk of the GEMM tile lies inside one
+// head and is stored as one contiguous 32-byte run of the attention layout;
+// the temporal segment is the plain 3D columns.  Segment order:
+//   sp.q sp.k sp.v | tm (3D) | fs.q fs.k fs.v
+struct QkvPad {
+  int32_t DP;       // padded head dim (64, 80 or 128)
+  int64_t SEG;      // H*DP
+  int64_t TMSEG;    // round_up(3D, 16)
+  int64_t Npad;     // 6*SEG + TMSEG
+  __host__ __device__ int64_t fs_base() const { return 3 * SEG + TMSEG; }
+};
+inline int qkv_head_pad(int64_t dh) { return dh <= 64 ? 64 : dh <= 80 ? 80 : dh <= 128 ? 128 : 0; }
+inline QkvPad qkv_pad_layout(int64_t D, int64_t H) {
+  QkvPad q;
+  q.DP = qkv_head_pad(D / H);
+  q.SEG = H * q.DP;
+  q.TMSEG = (3 * D + 15) / 16 * 16;
+  q.Npad = 6 * q.SEG + q.TMSEG;
+  return q;
+}
+
+int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int H, bool bf16,
                 cudaStream_t st);
 
 // stage profiler (vc_profile.cu)

@@ -170,10 +170,12 @@ int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h,
 // Weight pack (one-time).  raw = 3 branches x {gamma[D], beta[D], wq, wk, wv,
 // wo [D][D] row-major}.  Folding: (xhat*gamma + beta) @ W
 //   = xhat @ (diag(gamma) W) + beta @ W.
-// fp32 layout : Wqkv [D][9D] (x @ W orientation), bias [9D], Wo [3D][D]
-// bf16 layout : Wqkv^T [9D][D] (K-major for tcgen05), bias [9D] fp32,
-//               Wo^T [D][3D]
-// Column n of the 9D space = branch*3D + {q,k,v}*D + c.
+// fp32 layout : Wqkv [D][9D] (x @ W orientation), bias [9D], Wo [3D][D];
+//               column n of the 9D space = branch*3D + {q,k,v}*D + c.
+// bf16 layout : Wqkv^T [Npad][D] (K-major for tcgen05) in the head-padded
+//               column space of QkvPad (zero rows for the pad columns, so
+//               the GEMM writes exact zeros there), bias [Npad] fp32,
+//               Wo^T [D][3D].
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ const float* raw_branch(const float* raw, int b, int D) {
   return raw + (int64_t)b * (2 * (int64_t)D + 4 * (int64_t)D * D);
@@ -182,26 +184,52 @@ __device__ __forceinline__ const float* raw_w(const float* raw, int b, int which
   return raw_branch(raw, b, D) + 2 * (int64_t)D + (int64_t)which * D * D;  // which: 0 q,1 k,2 v,3 o
 }
 
+// Packed QKV column n -> (branch, which, source column c); false for a pad column.
+__device__ __forceinline__ bool qkv_source(int64_t n, int D, int H, bool padded, QkvPad q, int& b,
+                                           int& which, int& c) {
+  if (!padded) {
+    b = (int)(n / (3 * D)); which = (int)((n / D) % 3); c = (int)(n % D);
+    return true;
+  }
+  const int dh = D / H;
+  int64_t j;
+  if (n < 3 * q.SEG) { b = 0; which = (int)(n / q.SEG); j = n % q.SEG; }
+  else if (n < q.fs_base()) {
+    b = 1; j = n - 3 * q.SEG;
+    if (j >= 3 * D) return false;
+    which = (int)(j / D); c = (int)(j % D);
+    return true;
+  } else { b = 2; const int64_t r = n - q.fs_base(); which = (int)(r / q.SEG); j = r % q.SEG; }
+  const int h = (int)(j / q.DP), d = (int)(j % q.DP);
+  if (h >= H || d >= dh) return false;
+  c = h * dh + d;
+  return true;
+}
+
 template <typename T, bool KMAJOR>
-__global__ void pack_qkv_kernel(const float* __restrict__ raw, T* __restrict__ wqkv, int D) {
-  // one thread per (k, n) of the 9D x D matrix
-  const int64_t total = (int64_t)9 * D * D;
+__global__ void pack_qkv_kernel(const float* __restrict__ raw, T* __restrict__ wqkv, int D, int H,
+                                int64_t N, QkvPad q) {
+  // one thread per (k, n) of the N x D matrix
+  const int64_t total = N * D;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t n, k;
-    if (KMAJOR) { n = e / D; k = e % D; }      // output [9D][D], k fastest
-    else { k = e / (9 * (int64_t)D); n = e % (9 * (int64_t)D); }  // output [D][9D]
-    const int b = (int)(n / (3 * D)), which = (int)((n / D) % 3), c = (int)(n % D);
-    const float g = raw_branch(raw, b, D)[k];
-    const float wv = raw_w(raw, b, which, D)[k * D + c];
-    wqkv[e] = from_f32<T>(g * wv);
+    if (KMAJOR) { n = e / D; k = e % D; }  // output [N][D], k fastest
+    else { k = e / N; n = e % N; }         // output [D][N]
+    int b, which, c;
+    float v = 0.f;
+    if (qkv_source(n, D, H, KMAJOR, q, b, which, c))
+      v = raw_branch(raw, b, D)[k] * raw_w(raw, b, which, D)[k * D + c];
+    wqkv[e] = from_f32<T>(v);
   }
 }
 
-__global__ void pack_bias_kernel(const float* __restrict__ raw, float* __restrict__ bias, int D) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= 9 * D) return;
-  const int b = n / (3 * D), which = (n / D) % 3, c = n % D;
+__global__ void pack_bias_kernel(const float* __restrict__ raw, float* __restrict__ bias, int D,
+                                 int H, int64_t N, bool padded, QkvPad q) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  int b, which, c;
+  if (!qkv_source(n, D, H, padded, q, b, which, c)) { bias[n] = 0.f; return; }
   const float* beta = raw_branch(raw, b, D) + D;
   const float* W = raw_w(raw, b, which, D);
   double acc = 0.0;
@@ -222,17 +250,20 @@ __global__ void pack_o_kernel(const float* __restrict__ raw, T* __restrict__ wo,
   }
 }
 
-int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, bool bf16,
+int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int H, bool bf16,
                 cudaStream_t st) {
   const int blocks = 148 * 8;
+  const QkvPad q = qkv_pad_layout(D, H);
+  const int64_t N = bf16 ? q.Npad : 9 * (int64_t)D;
   if (bf16) {
-    pack_qkv_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wqkv, D);
+    if (q.DP == 0) { set_error("head dim %d unsupported on the bf16 path", D / H); return VC_ENOTSUP; }
+    pack_qkv_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wqkv, D, H, N, q);
     pack_o_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wo, D);
   } else {
-    pack_qkv_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wqkv, D);
+    pack_qkv_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wqkv, D, H, N, q);
     pack_o_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wo, D);
   }
-  pack_bias_kernel<<<(unsigned)cdiv(9 * D, 128), 128, 0, st>>>(raw, bias, D);
+  pack_bias_kernel<<<(unsigned)cdiv(N, 128), 128, 0, st>>>(raw, bias, D, H, N, bf16, q);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
