@@ -44,13 +44,15 @@ struct Cfg {
   static constexpr int QK_BYTES = BQ * DP * 2;         // one Q (or K) tile
   static constexpr int V_BYTES = DP * BKV * 2;         // one Vt tile (2 chunks of 64 keys)
   static constexpr int P_BYTES = BQ * BKV * 2;         // one P tile
+  static constexpr int KS = DP <= 80 ? 3 : 2;          // K and V ring depth
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + QK_BYTES;       // 2 stages
-  static constexpr int OFF_V = OFF_K + 2 * QK_BYTES;   // 2 stages
-  static constexpr int OFF_P = OFF_V + 2 * V_BYTES;    // 2 buffers
+  static constexpr int OFF_K = OFF_Q + QK_BYTES;       // KS stages
+  static constexpr int OFF_V = OFF_K + KS * QK_BYTES;  // KS stages
+  static constexpr int OFF_P = OFF_V + KS * V_BYTES;   // 2 buffers
   static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int KSTEPS = DP / 16;               // MMA K steps of S = Q K^T
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 // Byte offset, inside a Q/K tile, of the head-dim 16-chunk c; tiles are laid
@@ -72,17 +74,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
                    const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
   using CF = Cfg<DP>;
+  constexpr int KS = CF::KS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_empty = bars + 7;   // [2]
-  uint64_t* p_full = bars + 9;    // [2]
-  uint64_t* pv_done = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* k_full = bars + 1;            // [KS]  K tile landed
+  uint64_t* k_empty = k_full + KS;        // [KS]  S MMA done reading it
+  uint64_t* v_full = k_empty + KS;        // [KS]
+  uint64_t* v_empty = v_full + KS;        // [KS]  PV MMA done reading it
+  uint64_t* s_full = v_empty + KS;        // [2]   S in TMEM
+  uint64_t* s_empty = s_full + 2;         // [2]   softmax has read S
+  uint64_t* p_full = s_empty + 2;         // [2]   P in smem
+  uint64_t* pv_done = p_full + 2;         // [2]   PV MMA complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5;
   const int q0 = blockIdx.x * BQ;
@@ -94,14 +99,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmQ64); ptx::prefetch_tmap(&tmK64); ptx::prefetch_tmap(&tmV);
     if (CF::TAIL) { ptx::prefetch_tmap(&tmQ16); ptx::prefetch_tmap(&tmK16); }
     ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < KS; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&kv_full[i], 1);
-      ptx::mbar_init(&kv_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&s_empty[i], 128);
       ptx::mbar_init(&p_full[i], 128);
+      ptx::mbar_init(&pv_done[i], 1);
     }
-    ptx::mbar_init(pv_done, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
@@ -121,17 +130,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_load_4d(sQ + c * BQ * 128, &tmQ64, q_full, c * 64, h, q0, seq);
       if (CF::TAIL) ptx::tma_load_4d(sQ + CF::N64 * BQ * 128, &tmQ16, q_full, CF::N64 * 64, h, q0, seq);
       for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1;
-        ptx::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&kv_full[s], CF::QK_BYTES + CF::V_BYTES);
-        uint8_t* sK = smem + CF::OFF_K + s * CF::QK_BYTES;
-        uint8_t* sV = smem + CF::OFF_V + s * CF::V_BYTES;
+        const int s = j % KS;
+        const uint32_t ph = ((j / KS) & 1) ^ 1;
         const int k0 = j * BKV;
+        ptx::mbar_wait(&k_empty[s], ph);
+        ptx::mbar_arrive_expect_tx(&k_full[s], CF::QK_BYTES);
+        uint8_t* sK = smem + CF::OFF_K + s * CF::QK_BYTES;
         for (int c = 0; c < CF::N64; ++c)
-          ptx::tma_load_4d(sK + c * BKV * 128, &tmK64, &kv_full[s], c * 64, h, k0, seq);
-        if (CF::TAIL) ptx::tma_load_4d(sK + CF::N64 * BKV * 128, &tmK16, &kv_full[s], CF::N64 * 64, h, k0, seq);
-        ptx::tma_load_4d(sV, &tmV, &kv_full[s], k0, 0, h, seq);
-        ptx::tma_load_4d(sV + DP * 128, &tmV, &kv_full[s], k0 + 64, 0, h, seq);
+          ptx::tma_load_4d(sK + c * BKV * 128, &tmK64, &k_full[s], c * 64, h, k0, seq);
+        if (CF::TAIL) ptx::tma_load_4d(sK + CF::N64 * BKV * 128, &tmK16, &k_full[s], CF::N64 * 64, h, k0, seq);
+        ptx::mbar_wait(&v_empty[s], ph);
+        ptx::mbar_arrive_expect_tx(&v_full[s], CF::V_BYTES);
+        uint8_t* sV = smem + CF::OFF_V + s * CF::V_BYTES;
+        ptx::tma_load_4d(sV, &tmV, &v_full[s], k0, 0, h, seq);
+        ptx::tma_load_4d(sV + DP * 128, &tmV, &v_full[s], k0 + 64, 0, h, seq);
       }
     }
   } else if (warp == 1) {
@@ -141,36 +153,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t aQ = ptx::smem_u32(smem + CF::OFF_Q);
     ptx::mbar_wait(q_full, 0);
     auto issue_s = [&](int j) {
-      const int s = j & 1;
-      ptx::mbar_wait(&kv_full[s], (j >> 1) & 1);
+      const int s = j & 1, ks = j % KS;
+      ptx::mbar_wait(&k_full[ks], (j / KS) & 1);
       ptx::mbar_wait(&s_empty[s], ((j >> 1) & 1) ^ 1);
       ptx::fence_after_sync();
       if (ptx::elect_one()) {
-        const uint32_t aK = ptx::smem_u32(smem + CF::OFF_K + s * CF::QK_BYTES);
+        const uint32_t aK = ptx::smem_u32(smem + CF::OFF_K + ks * CF::QK_BYTES);
 #pragma unroll
         for (int c = 0; c < CF::KSTEPS; ++c)
           ptx::mma_bf16_ss(tS + s * BKV, qk_desc<DP>(aQ, c), qk_desc<DP>(aK, c), idS, c > 0);
         ptx::mma_commit(&s_full[s]);
+        ptx::mma_commit(&k_empty[ks]);
       }
       __syncwarp();
     };
     issue_s(0);
     for (int j = 0; j < n_tiles; ++j) {
       if (j + 1 < n_tiles) issue_s(j + 1);
-      const int s = j & 1;
+      const int s = j & 1, ks = j % KS;
+      ptx::mbar_wait(&v_full[ks], (j / KS) & 1);
       ptx::mbar_wait(&p_full[s], (j >> 1) & 1);
       ptx::fence_after_sync();
       if (ptx::elect_one()) {
         const uint32_t aP = ptx::smem_u32(smem + CF::OFF_P + s * CF::P_BYTES);
-        const uint32_t aV = ptx::smem_u32(smem + CF::OFF_V + s * CF::V_BYTES);
+        const uint32_t aV = ptx::smem_u32(smem + CF::OFF_V + ks * CF::V_BYTES);
 #pragma unroll
         for (int c = 0; c < BKV / 16; ++c) {
           const uint64_t ad = ptx::smem_desc(aP + (c >> 2) * (BQ * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
           const uint64_t bd = ptx::smem_desc(aV + (c >> 2) * (DP * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
           ptx::mma_bf16_ss(tO, ad, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
         }
-        ptx::mma_commit(&kv_empty[s]);
-        ptx::mma_commit(pv_done);
+        ptx::mma_commit(&v_empty[ks]);
+        ptx::mma_commit(&pv_done[s]);
       }
       __syncwarp();
     }
@@ -227,23 +241,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         alpha = ptx::ex2(m_used - mx);  // 0 on the first tile
         m_used = mx;
       }
-      const float neg_m = -m_used;
-      float s8[8];
+      // p = 2^(s*scale - m): FFMA2 (two logits per instruction) + MUFU.EX2;
+      // row sum in four FADD2 partials
+      const float2 sc2 = make_float2(scale, scale), nm2 = make_float2(-m_used, -m_used);
+      float2 s4[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+      for (int i = 0; i < 4; ++i) s4[i] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) {
-        v[i] = ptx::ex2(fmaf(v[i], scale, neg_m));
-        s8[i & 7] += v[i];
+      for (int i = 0; i < BKV; i += 2) {
+        float2 t = ptx::ffma2(make_float2(v[i], v[i + 1]), sc2, nm2);
+        t.x = ptx::ex2(t.x);
+        t.y = ptx::ex2(t.y);
+        v[i] = t.x;
+        v[i + 1] = t.y;
+        s4[(i >> 1) & 3] = ptx::fadd2(s4[(i >> 1) & 3], t);
       }
-      const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+      const float2 s2 = ptx::fadd2(ptx::fadd2(s4[0], s4[1]), ptx::fadd2(s4[2], s4[3]));
+      const float sum = s2.x + s2.y;
       l = l * alpha + sum;
-      // O (in TMEM) holds P(j-1) V(j-1) only after that MMA completes; the P
-      // buffer s was last read by PV(j-2), also complete by then.
-      if (j > 0) {
-        ptx::mbar_wait(pv_done, (j - 1) & 1);
+      // PV(i) arrives on pv_done[i & 1] (its completion #(i >> 1) there). The
+      // P buffer s was last read by PV(j-2); O holds P(j-1) V(j-1) only once
+      // PV(j-1) completes, which matters only if O must be rescaled -- so the
+      // common case lets PV(j-1) run under this tile's softmax.
+      if (j >= 2) ptx::mbar_wait(&pv_done[s], ((j - 2) >> 1) & 1);
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        ptx::mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         ptx::fence_after_sync();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        {
 #pragma unroll
           for (int c = 0; c < DP / 16; ++c) {
             uint32_t r[16];
@@ -258,23 +282,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // P -> bf16 -> smem, SW128 K-major: chunk of 64 keys, row pitch 128 B,
       // 16-byte unit u of row r stored at u ^ (r & 7).
-      uint8_t* sP = smem + CF::OFF_P + s * CF::P_BYTES;
+      const uint32_t sP = ptx::smem_u32(smem + CF::OFF_P + s * CF::P_BYTES);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint8_t* rowp = sP + c * (BQ * 128) + row * 128;
+        const uint32_t rowp = sP + c * (BQ * 128) + row * 128;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const float* pv = v + c * 64 + u * 8;
-          uint4 w;
-          __nv_bfloat162 b0 = __floats2bfloat162_rn(pv[0], pv[1]);
-          __nv_bfloat162 b1 = __floats2bfloat162_rn(pv[2], pv[3]);
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(pv[4], pv[5]);
-          __nv_bfloat162 b3 = __floats2bfloat162_rn(pv[6], pv[7]);
-          w.x = *reinterpret_cast<uint32_t*>(&b0);
-          w.y = *reinterpret_cast<uint32_t*>(&b1);
-          w.z = *reinterpret_cast<uint32_t*>(&b2);
-          w.w = *reinterpret_cast<uint32_t*>(&b3);
-          *reinterpret_cast<uint4*>(rowp + ((u ^ (row & 7)) << 4)) = w;
+          ptx::sts128(rowp + ((u ^ (row & 7)) << 4), ptx::bf16x2(pv[0], pv[1]), ptx::bf16x2(pv[2], pv[3]),
+                      ptx::bf16x2(pv[4], pv[5]), ptx::bf16x2(pv[6], pv[7]));
         }
       }
       ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_arrive(&p_full[s]);
     }
     // ---- epilogue: O / l -> bf16 -> out[row][col_off + h*dh + d], d < dh ----
-    ptx::mbar_wait(pv_done, (n_tiles - 1) & 1);
+    ptx::mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     ptx::fence_after_sync();
     const int qi = q0 + row;
     const float inv = 1.f / l;

@@ -95,15 +95,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_attn_tc(a, sc.sp.q, sc.sp.k, sc.sp.vt, (int)F, Lv, Lv, wl.Lv_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_spatial");
-  {
-    AttnArgs<bf, bf> a{};
-    a.q = tm + 0 * D; a.ldq = 3 * D; a.q_seq_stride = 1; a.q_tok_stride = Lv;
-    a.k = tm + 1 * D; a.v = tm + 2 * D; a.ldk = 3 * D; a.k_seq_stride = 1; a.k_tok_stride = Lv;
-    a.o = acat + 1 * D; a.ldo = 3 * D; a.o_seq_stride = 1; a.o_tok_stride = Lv;
-    a.n_seq = (int)Lv; a.len_q = (int)F; a.len_k = (int)F; a.heads = (int)H; a.dh = (int)dh;
-    a.scale_log2 = scale_log2;
-    VC_TRY(launch_attn_simt(a, st));
-  }
+  VC_TRY((launch_temporal_attn<bf, bf>(tm, 3 * D, D, acat + D, 3 * D, (int)F, (int)Lv, (int)H, (int)dh, st)));
   profile_mark(st, "attn_temporal");
   {
     AttnTcParams a{};

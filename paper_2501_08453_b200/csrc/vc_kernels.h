@@ -17,6 +17,12 @@ int launch_gemm_f32(const GemmF32Args& g, cudaStream_t st);
 template <typename T, typename OutT>
 int launch_attn_simt(const AttnArgs<T, OutT>& a, cudaStream_t st);
 
+// Temporal branch: q/k/v of row r at qkv[r*ld + {0, D, 2D}], sequence l =
+// rows {f*Lv + l}; output o[r*ldo + h*dh + d].  (vc_attn_temporal.cu)
+template <typename T, typename OutT>
+int launch_temporal_attn(const T* qkv, int64_t ld, int64_t D, OutT* o, int64_t ldo, int F, int Lv,
+                         int H, int dh, cudaStream_t st);
+
 template <typename OutT>
 int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
                    cudaStream_t st);
