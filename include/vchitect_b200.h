@@ -142,6 +142,47 @@ VC_API int vc_gemm_bf16(const void* a_dev, int64_t lda, const void* b_dev,
                         const float* resid_dev, float* out_dev, int64_t ldo,
                         int64_t M, int32_t N, int32_t K, void* stream);
 
+/* ---- Sequence parallelism (the paper's hybrid-parallel scheme) ----------
+ * Spatial shard axis, head-parallel (Ulysses) attention, separate text
+ * placement: executor.py:561-626 (run_sp_iteration stage 3) with the two
+ * all-to-alls of _branch_head_parallel (executor.py:332-413). Rank r holds
+ * visual rows [vb[r], vb[r+1]) of every frame, vb = contiguous_bounds(Lv, P)
+ * (executor.py:187-191), and the whole prompt. The host runs
+ *   stage1 -> all_to_all(send1 -> recv1) -> stage2 -> all_to_all(send2 ->
+ *   recv2) -> stage3
+ * with per-peer counts from vc_sp_exchange_elems (bf16 elements). bf16 only. */
+typedef struct vc_sp_plan {
+  vc_block_shape shape; /* global block shape (dtype must be VC_DTYPE_BF16) */
+  int32_t nranks;       /* P: sp_size */
+  int32_t rank;
+} vc_sp_plan;
+
+/* executor.py:517-529 validity: P <= Lv, H % P == 0 (P > 1). */
+VC_API int vc_sp_check(const vc_sp_plan* plan);
+/* vbounds[0..P] = contiguous_bounds(Lv, P) (executor.py:187-191). */
+VC_API int vc_sp_bounds(const vc_sp_plan* plan, int32_t* vbounds);
+VC_API size_t vc_sp_workspace_bytes(const vc_sp_plan* plan);
+/* which: 0 send1 to peer, 1 recv1 from peer, 2 send2 to peer, 3 recv2 from
+ * peer. -1 on error. */
+VC_API int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which,
+                                    int32_t peer);
+/* x_local [F][vc_r][D] fp32, prompt [Lt][D] fp32 -> send1 (bf16). */
+VC_API int vc_sp_stage1(const vc_sp_plan* plan, const void* packed_dev,
+                        const float* x_local_dev, const float* prompt_dev,
+                        void* send1_dev, void* workspace_dev,
+                        size_t workspace_bytes, void* stream);
+/* recv1 -> head-group attention -> send2 (bf16). */
+VC_API int vc_sp_stage2(const vc_sp_plan* plan, const void* packed_dev,
+                        const void* recv1_dev, void* send2_dev,
+                        void* workspace_dev, size_t workspace_bytes,
+                        void* stream);
+/* recv2 -> O projection (+ x_local if add_residual) -> out_local fp32. */
+VC_API int vc_sp_stage3(const vc_sp_plan* plan, const void* packed_dev,
+                        const void* recv2_dev, const float* x_local_dev,
+                        float* out_local_dev, int add_residual,
+                        void* workspace_dev, size_t workspace_bytes,
+                        void* stream);
+
 /* Stage profiler (bench accounting, not used on the timed path): when
  * enabled, vc_block_forward records a CUDA event after each of its kernels,
  * synchronises at the end of the call and accumulates per-stage device time

@@ -24,6 +24,10 @@ class BlockShape(C.Structure):
                 ("dim", C.c_int32), ("heads", C.c_int32), ("dtype", C.c_int32)]
 
 
+class SpPlan(C.Structure):
+    _fields_ = [("shape", BlockShape), ("nranks", C.c_int32), ("rank", C.c_int32)]
+
+
 # name -> (restype, argtypes); mirrors include/vchitect_b200.h one to one.
 _p, _f, _i32, _i64, _sz, _d = C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_size_t, C.c_double
 _S = C.POINTER(BlockShape)
@@ -44,6 +48,13 @@ SIGNATURES = {
     "vc_unembed_frames": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32, _p]),
     "vc_gemm_bf16": (C.c_int, [_p, _i64, _p, _i64, _p, _p, _p, _i64, _i64, _i32, _i32, _p]),
     "vc_block_forward_launches": (C.c_int, [_S]),
+    "vc_sp_check": (C.c_int, [C.POINTER(SpPlan)]),
+    "vc_sp_bounds": (C.c_int, [C.POINTER(SpPlan), C.POINTER(C.c_int32)]),
+    "vc_sp_workspace_bytes": (_sz, [C.POINTER(SpPlan)]),
+    "vc_sp_exchange_elems": (_i64, [C.POINTER(SpPlan), _i32, _i32]),
+    "vc_sp_stage1": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _p, _sz, _p]),
+    "vc_sp_stage2": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _sz, _p]),
+    "vc_sp_stage3": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, C.c_int, _p, _sz, _p]),
     "vc_profile_enable": (C.c_int, [C.c_int]),
     "vc_profile_reset": (None, []),
     "vc_profile_read": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int32, C.c_char_p, C.c_size_t]),

@@ -302,7 +302,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_after_sync();
     const int qi = q0 + row;
     const float inv = 1.f / l;
-    __nv_bfloat16* orow = qi < p.Lq ? p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off + (int64_t)h * p.dh : nullptr;
+    __nv_bfloat16* orow = nullptr;
+    if (qi < p.Lq) {
+      if (p.spo.P == 0) {
+        orow = p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off + (int64_t)h * p.dh;
+      } else {  // sequence-parallel: straight into the all-to-all #2 send buffer
+        const int f = p.spo.branch == 0 ? seq : qi / p.spo.Lv;
+        const int lpos = p.spo.branch == 0 ? qi : qi - f * p.spo.Lv;
+        int r = 0;
+        while (r + 1 < p.spo.P && p.spo.vb[r + 1] <= lpos) ++r;
+        const int vc = p.spo.vb[r + 1] - p.spo.vb[r];
+        const int64_t Mr = (int64_t)p.spo.F * vc;
+        orow = p.out + p.spo.base[r] + (p.spo.branch * Mr + (int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg +
+               (int64_t)h * p.dh;
+      }
+    }
 #pragma unroll
     for (int c = 0; c < DP / 16; ++c) {
       uint32_t r[16];

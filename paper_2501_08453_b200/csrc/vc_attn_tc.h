@@ -4,6 +4,18 @@
 
 namespace vc {
 
+// Sequence-parallel output remap (all-to-all #2 send layout, executor.py:395-412):
+// query (frame f, position l) is owned by rank r with vb[r] <= l < vb[r+1]; its
+// head-group output row goes to send2[base[r] + (branch*M_r + f*vc_r + l - vb[r]) * Dg].
+struct SpOutMap {
+  int32_t P;         // 0: disabled (plain output rows)
+  int32_t branch;    // 0 spatial, 1 full sequence
+  int32_t F, Lv;
+  int64_t Dg;        // Hg * dh
+  int32_t vb[17];
+  int64_t base[17];
+};
+
 struct AttnTcParams {
   int32_t Lq, Lk, H, dh;
   int32_t n_bias;       // keys [0, n_bias) get + bias_log2 (deduplicated anchored text)
@@ -13,6 +25,7 @@ struct AttnTcParams {
   int64_t ld_out;
   int64_t col_off;
   int64_t out_seq_rows;
+  SpOutMap spo;
 };
 
 // Padded head dim the tensor-core kernel uses for dh (0: unsupported).

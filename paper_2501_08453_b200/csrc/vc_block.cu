@@ -79,15 +79,19 @@ static int check_shape(const vc_block_shape* s, Dims* d) {
 struct PackedLayout {
   size_t wqkv, bias, wo, total;
 };
-static PackedLayout packed_layout(const Dims& d) {
-  const size_t es = d.bf16 ? 2 : 4;
+void packed_offsets(int64_t D, int64_t H, bool bf16, size_t* wqkv, size_t* bias, size_t* wo,
+                    size_t* total) {
+  const size_t es = bf16 ? 2 : 4;
   // bf16: head-padded QKV column space (vc_kernels.h QkvPad); fp32: plain 9D
-  const int64_t nq = d.bf16 ? qkv_pad_layout(d.D, d.H).Npad : 9 * d.D;
+  const int64_t nq = bf16 ? qkv_pad_layout(D, H).Npad : 9 * D;
+  *wqkv = 0;
+  *bias = align_up(*wqkv + (size_t)nq * D * es, 1024);
+  *wo = align_up(*bias + (size_t)nq * 4, 1024);
+  *total = align_up(*wo + (size_t)3 * D * D * es, 1024);
+}
+static PackedLayout packed_layout(const Dims& d) {
   PackedLayout p;
-  p.wqkv = 0;
-  p.bias = align_up(p.wqkv + (size_t)nq * d.D * es, 1024);
-  p.wo = align_up(p.bias + (size_t)nq * 4, 1024);
-  p.total = align_up(p.wo + (size_t)3 * d.D * d.D * es, 1024);
+  packed_offsets(d.D, d.H, d.bf16, &p.wqkv, &p.bias, &p.wo, &p.total);
   return p;
 }
 

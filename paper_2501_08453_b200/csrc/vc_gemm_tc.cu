@@ -120,7 +120,22 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
     const int64_t r = b == 0 ? n : n - q.fs_base();
     const int which = (int)(r / q.SEG);
     const int64_t jj = r - which * q.SEG;
-    const int h = (int)(jj / q.DP), d0 = (int)(jj % q.DP);  // 16 | DP: the chunk is inside head h
+    const int hg = (int)(jj / q.DP), d0 = (int)(jj % q.DP);  // 16 | DP: the chunk is inside head hg
+    if (s.mode == 1) {  // sequence-parallel send layout
+      const int g = hg / s.Hg, hl = hg - g * s.Hg;
+      const int64_t rowlen = (int64_t)s.Hg * q.DP;
+      __nv_bfloat16* o = s.send + g * 6 * s.send_rows * rowlen +
+                         (((b == 0 ? 0 : 3) + which) * s.send_rows + m) * rowlen + hl * q.DP + d0;
+      uint4 a, c;
+      a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);
+      a.z = pack_bf16x2(v[4], v[5]); a.w = pack_bf16x2(v[6], v[7]);
+      c.x = pack_bf16x2(v[8], v[9]); c.y = pack_bf16x2(v[10], v[11]);
+      c.z = pack_bf16x2(v[12], v[13]); c.w = pack_bf16x2(v[14], v[15]);
+      reinterpret_cast<uint4*>(o)[0] = a;
+      reinterpret_cast<uint4*>(o)[1] = c;
+      return;
+    }
+    const int h = hg - s.head_base;
     const BranchOut& bo = b == 0 ? s.sp : s.fs;
     int64_t qrow, krow, seq, key;
     qkv_rows(s, b, m, qrow, krow, seq, key);

@@ -20,11 +20,19 @@ struct BranchOut {
 struct QkvScatter {
   QkvPad pad;         // head-padded column space (vc_kernels.h)
   int64_t D, Lv, Lt;
-  int32_t H;
+  int32_t H;          // heads of the destination layout
+  int32_t head_base;  // first head of this GEMM's columns (stored as h - head_base)
   int64_t n_base;     // column of this GEMM's n=0 in the padded space
   int32_t text_rows;  // rows are prompt rows (full-sequence keys 0..Lt-1)
   BranchOut sp, fs;
   __nv_bfloat16* tm;  // temporal branch, plain [row][3D]
+  // mode 1 (sequence-parallel send): spatial / full-seq Q, K, V of local row m
+  // and head h go to send[g][b'][which][m][h % Hg][DP], g = h / Hg (head group
+  // owner), b' = 0 spatial / 1 full sequence; all-to-all #1 of executor.py:344.
+  int32_t mode;
+  int32_t Hg;
+  int64_t send_rows;  // local rows M_r
+  __nv_bfloat16* send;
 };
 
 struct GemmTcParams {

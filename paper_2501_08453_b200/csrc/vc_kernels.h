@@ -56,6 +56,9 @@ inline QkvPad qkv_pad_layout(int64_t D, int64_t H) {
 
 int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int H, bool bf16,
                 cudaStream_t st);
+// Byte offsets inside the packed weight buffer (vc_block.cu).
+void packed_offsets(int64_t D, int64_t H, bool bf16, size_t* wqkv, size_t* bias, size_t* wo,
+                    size_t* total);
 
 // stage profiler (vc_profile.cu)
 bool profile_on();

@@ -1,0 +1,347 @@
+// Sequence-parallel block forward: the three rank-local stages around the two
+// all-to-alls of the paper's memory-efficient hybrid-parallel scheme
+// (executor.py:561-626, spatial shard axis, head-parallel attention,
+// "separate" text placement).  The collectives themselves are NCCL
+// all_to_all_single calls issued by the host (paper_2501_08453_b200/sp.py);
+// this file owns every byte layout on either side of them.
+//
+// Rank r holds visual rows [vb[r], vb[r+1]) of every frame (vb =
+// contiguous_bounds(Lv, P), executor.py:187-191) and the whole prompt
+// (text is static, anchored context any rank can regenerate; executor.py
+// docstring).  Head group g = heads [g*H/P, (g+1)*H/P) is owned by rank g.
+//
+//   stage 1 (rank r): LN + QKV GEMM of the local rows; the epilogue writes the
+//       spatial / full-seq q, k, v straight into the a2a #1 send layout
+//       send1[g][b'][which][m][Hg][DP]; temporal branch is rank-local.
+//   a2a #1 (NCCL)
+//   stage 2 (rank g): unpack into the attention layouts for the Hg heads of
+//       the group (full frames / full sequence), text K/V of the group's heads
+//       from the local prompt copy, tcgen05 attention whose epilogue writes
+//       the a2a #2 send layout send2[r][b'][m][Dg] (executor.py:395-412).
+//   a2a #2 (NCCL)
+//   stage 3 (rank r): gather the 2P head-group column blocks into [A_sp|A_tm|
+//       A_fs] and run the O GEMM + residual for the local rows.
+#include <math.h>
+
+#include "vc_attn_tc.h"
+#include "vc_gemm_tc.h"
+#include "vc_kernels.h"
+
+namespace vc {
+
+namespace {
+
+inline size_t aup(size_t v) { return (v + 1023) / 1024 * 1024; }
+
+struct Sp {
+  int64_t F, Lv, Lt, D, H, dh, Nv, P, rank, Hg, Dg, DP, Lv_ld, Lk_ld;
+  int32_t vb[17];
+  int64_t M[16];       // local rows F*vc_r per rank
+  int64_t s1_off[17];  // element offsets of per-peer blocks: recv1 (by source rank)
+  int64_t s2_off[17];  // send2 (by destination rank)
+  QkvPad pad;
+};
+
+int sp_make(const vc_sp_plan* pl, Sp* o) {
+  if (!pl) { set_error("null plan"); return VC_EINVAL; }
+  const vc_block_shape& s = pl->shape;
+  VC_TRY(vc_block_shape_check(&s));
+  if (s.dtype != VC_DTYPE_BF16) { set_error("sequence parallelism runs the bf16 path"); return VC_ENOTSUP; }
+  const int P = pl->nranks;
+  if (P < 1 || P > 16 || pl->rank < 0 || pl->rank >= P) {
+    set_error("bad rank %d of %d (1..16 ranks)", pl->rank, P);
+    return VC_EINVAL;
+  }
+  if (P > s.visual_len) {  // executor.py:521-524
+    set_error("cannot spread %d visual tokens per frame over %d devices", s.visual_len, P);
+    return VC_EINVAL;
+  }
+  if (P > 1 && s.heads % P != 0) {  // executor.py:525-529
+    set_error("head-parallel attention needs sp_size to divide %d heads, got %d", s.heads, P);
+    return VC_EINVAL;
+  }
+  Sp& x = *o;
+  x.F = s.frames; x.Lv = s.visual_len; x.Lt = s.text_len; x.D = s.dim; x.H = s.heads;
+  x.dh = x.D / x.H; x.Nv = x.F * x.Lv; x.P = P; x.rank = pl->rank;
+  x.Hg = x.H / P; x.Dg = x.Hg * x.dh;
+  x.pad = qkv_pad_layout(x.D, x.H);
+  x.DP = x.pad.DP;
+  x.Lv_ld = round_up(x.Lv, 8);
+  x.Lk_ld = round_up(x.Lt + x.Nv, 8);
+  for (int r = 0; r <= P; ++r) x.vb[r] = (int32_t)((int64_t)r * x.Lv / P);  // contiguous_bounds
+  x.s1_off[0] = 0; x.s2_off[0] = 0;
+  for (int r = 0; r < P; ++r) {
+    x.M[r] = x.F * (x.vb[r + 1] - x.vb[r]);
+    x.s1_off[r + 1] = x.s1_off[r] + 6 * x.M[r] * x.Hg * x.DP;
+    x.s2_off[r + 1] = x.s2_off[r] + 2 * x.M[r] * x.Dg;
+  }
+  return VC_OK;
+}
+
+struct SpWs {
+  size_t xhat, tm, qsp, ksp, vtsp, qfs, kfs, vtfs, acat, total;
+};
+SpWs sp_ws(const Sp& x) {
+  SpWs w;
+  const int64_t Mr = x.M[x.rank];
+  const size_t qk = (size_t)x.Hg * x.DP * 2;
+  size_t o = 0;
+  w.xhat = o; o = aup(o + (size_t)(Mr + x.Lt) * x.D * 2);
+  w.tm = o; o = aup(o + (size_t)Mr * 3 * x.D * 2);
+  w.qsp = o; o = aup(o + (size_t)x.Nv * qk);
+  w.ksp = o; o = aup(o + (size_t)x.Nv * qk);
+  w.vtsp = o; o = aup(o + (size_t)x.F * x.Hg * x.DP * x.Lv_ld * 2);
+  w.qfs = o; o = aup(o + (size_t)x.Nv * qk);
+  w.kfs = o; o = aup(o + (size_t)(x.Lt + x.Nv) * qk);
+  w.vtfs = o; o = aup(o + (size_t)x.Hg * x.DP * x.Lk_ld * 2);
+  w.acat = o; o = aup(o + (size_t)Mr * 3 * x.D * 2);
+  w.total = o;
+  return w;
+}
+
+struct PackedPtrs {
+  const __nv_bfloat16* wqkv;
+  const float* bias;
+  const __nv_bfloat16* wo;
+};
+PackedPtrs packed_ptrs(const Sp& x, const void* packed) {
+  size_t wqkv, bias, wo, total;
+  packed_offsets(x.D, x.H, true, &wqkv, &bias, &wo, &total);
+  const char* p = (const char*)packed;
+  return PackedPtrs{(const __nv_bfloat16*)(p + wqkv), (const float*)(p + bias), (const __nv_bfloat16*)(p + wo)};
+}
+
+struct UnpackArgs {
+  const __nv_bfloat16* recv;
+  int32_t P, F, Lv, Lt, Hg, DP;
+  int32_t vb[17];
+  int64_t off[17];  // recv1 block offsets by source rank
+  int64_t groups[17];  // prefix count of 32-row groups by source rank
+  __nv_bfloat16 *qsp, *ksp, *vtsp, *qfs, *kfs, *vtfs;
+  int64_t Lv_ld, Lk_ld;
+};
+
+// recv1[r][b'][which][m][Hg][DP] -> attention layouts of this head group.
+// One warp per 32 consecutive local rows of one (source, b', which) block;
+// lane = row. Q/K rows are copied whole (16-byte vectors); V is transposed
+// (lanes write consecutive keys of one head dim: coalesced).
+__global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int rowlen = a.Hg * a.DP;
+  for (int64_t w = gw; w < a.groups[a.P]; w += nw) {
+    int r = 0;
+    while (w >= a.groups[r + 1]) ++r;
+    const int vc = a.vb[r + 1] - a.vb[r];
+    const int64_t Mr = (int64_t)a.F * vc;
+    const int64_t gpb = (Mr + 31) / 32;  // row groups per (b', which) block
+    const int64_t wl = w - a.groups[r];
+    const int blk = (int)(wl / gpb);  // b'*3 + which
+    const int64_t m = (wl - blk * gpb) * 32 + lane;
+    if (m >= Mr) continue;
+    const int bp = blk / 3, which = blk - bp * 3;
+    const int f = (int)(m / vc), l = a.vb[r] + (int)(m - (int64_t)f * vc);
+    const __nv_bfloat16* src = a.recv + a.off[r] + ((int64_t)blk * Mr + m) * rowlen;
+    const int64_t tok = (int64_t)f * a.Lv + l;  // visual token index
+    if (which < 2) {
+      __nv_bfloat16* dst;
+      if (bp == 0) dst = (which == 0 ? a.qsp : a.ksp) + tok * rowlen;
+      else dst = which == 0 ? a.qfs + tok * rowlen : a.kfs + (a.Lt + tok) * rowlen;
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      for (int i = 0; i < rowlen / 8; ++i) d4[i] = s4[i];
+    } else {
+      __nv_bfloat16* base;
+      int64_t ld, key;
+      if (bp == 0) { base = a.vtsp + (int64_t)f * a.Hg * a.DP * a.Lv_ld; ld = a.Lv_ld; key = l; }
+      else { base = a.vtfs; ld = a.Lk_ld; key = a.Lt + tok; }
+      for (int i = 0; i < rowlen / 8; ++i) {
+        const uint4 v = reinterpret_cast<const uint4*>(src)[i];
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) base[(int64_t)(i * 8 + k) * ld + key] = e[k];  // row hl*DP+d of Vt
+      }
+    }
+  }
+}
+
+// recv2[g][b'][m][Dg] -> acat[m][b'*2D + g*Dg + c]  (b'=0 spatial cols [0,D), b'=1 full-seq [2D,3D))
+__global__ void sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv, __nv_bfloat16* __restrict__ acat,
+                                  int P, int64_t Mr, int64_t Dg, int64_t D) {
+  const int64_t words = Dg / 2;  // Dg even (dh even)
+  const int64_t total = (int64_t)P * 2 * Mr * words;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t wi = e % words;
+    const int64_t row = e / words;  // (g*2 + b')*Mr + m
+    const int64_t m = row % Mr;
+    const int64_t gb = row / Mr;
+    const int g = (int)(gb / 2), bp = (int)(gb % 2);
+    const uint32_t v = reinterpret_cast<const uint32_t*>(recv + row * Dg)[wi];
+    reinterpret_cast<uint32_t*>(acat + m * 3 * D + bp * 2 * D + (int64_t)g * Dg)[wi] = v;
+  }
+}
+
+}  // namespace
+
+}  // namespace vc
+
+using namespace vc;
+
+extern "C" {
+
+int vc_sp_check(const vc_sp_plan* plan) {
+  Sp x;
+  return sp_make(plan, &x);
+}
+
+int vc_sp_bounds(const vc_sp_plan* plan, int32_t* vbounds) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x));
+  for (int r = 0; r <= x.P; ++r) vbounds[r] = x.vb[r];
+  return VC_OK;
+}
+
+size_t vc_sp_workspace_bytes(const vc_sp_plan* plan) {
+  Sp x;
+  if (sp_make(plan, &x) != VC_OK) return 0;
+  return sp_ws(x).total;
+}
+
+int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which, int32_t peer) {
+  Sp x;
+  if (sp_make(plan, &x) != VC_OK || peer < 0 || peer >= x.P) return -1;
+  const int64_t me = x.M[x.rank];
+  switch (which) {
+    case 0: return 6 * me * x.Hg * x.DP;           // send1 to peer (my rows, peer's heads)
+    case 1: return 6 * x.M[peer] * x.Hg * x.DP;    // recv1 from peer (peer's rows, my heads)
+    case 2: return 2 * x.M[peer] * x.Dg;           // send2 to peer (peer's rows, my heads)
+    case 3: return 2 * me * x.Dg;                  // recv2 from peer (my rows, peer's heads)
+  }
+  return -1;
+}
+
+int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_local, const float* prompt,
+                 void* send1, void* ws, size_t ws_bytes, void* stream) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x));
+  const SpWs w = sp_ws(x);
+  if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* W = (char*)ws;
+  typedef __nv_bfloat16 bf;
+  const PackedPtrs pp = packed_ptrs(x, packed);
+  const int64_t Mr = x.M[x.rank];
+  const int vc = x.vb[x.rank + 1] - x.vb[x.rank];
+  bf* xhat = (bf*)(W + w.xhat);
+  bf* tm = (bf*)(W + w.tm);
+  bf* acat = (bf*)(W + w.acat);
+  VC_TRY(launch_ln_rows<bf>(x_local, Mr, prompt, x.Lt, (int)x.D, xhat, st));
+  profile_mark(st, "sp_ln");
+  if (Mr > 0) {
+    GemmTcParams g{};
+    g.M = Mr; g.N = (int)x.pad.Npad; g.K = (int)x.D; g.bias = pp.bias;
+    QkvScatter& s = g.qkv;
+    s.pad = x.pad; s.D = x.D; s.Lv = x.Lv; s.Lt = x.Lt; s.H = (int)x.H; s.tm = tm;
+    s.mode = 1; s.Hg = (int)x.Hg; s.send_rows = Mr; s.send = (bf*)send1;
+    VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
+    profile_mark(st, "sp_qkv_gemm");
+    // temporal branch is rank-local: sequence = local position, tokens = frames (stride vc)
+    VC_TRY((launch_temporal_attn<bf, bf>(tm, 3 * x.D, x.D, acat + x.D, 3 * x.D, (int)x.F, vc, (int)x.H,
+                                         (int)x.dh, st)));
+    profile_mark(st, "sp_attn_temporal");
+  }
+  return VC_OK;
+}
+
+int vc_sp_stage2(const vc_sp_plan* plan, const void* packed, const void* recv1, void* send2, void* ws,
+                 size_t ws_bytes, void* stream) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x));
+  const SpWs w = sp_ws(x);
+  if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* W = (char*)ws;
+  typedef __nv_bfloat16 bf;
+  const PackedPtrs pp = packed_ptrs(x, packed);
+  const int64_t Mr = x.M[x.rank];
+  bf* xhat = (bf*)(W + w.xhat);
+  BranchOut sp{(bf*)(W + w.qsp), (bf*)(W + w.ksp), (bf*)(W + w.vtsp), x.Lv_ld};
+  BranchOut fs{(bf*)(W + w.qfs), (bf*)(W + w.kfs), (bf*)(W + w.vtfs), x.Lk_ld};
+  {
+    UnpackArgs a{};
+    a.recv = (const bf*)recv1; a.P = (int)x.P; a.F = (int)x.F; a.Lv = (int)x.Lv; a.Lt = (int)x.Lt;
+    a.Hg = (int)x.Hg; a.DP = (int)x.DP;
+    a.groups[0] = 0;
+    for (int r = 0; r <= x.P; ++r) { a.vb[r] = x.vb[r]; a.off[r] = x.s1_off[r]; }
+    for (int r = 0; r < x.P; ++r) a.groups[r + 1] = a.groups[r] + 6 * cdiv(x.M[r], 32);
+    a.qsp = sp.q; a.ksp = sp.k; a.vtsp = sp.vt; a.qfs = fs.q; a.kfs = fs.k; a.vtfs = fs.vt;
+    a.Lv_ld = x.Lv_ld; a.Lk_ld = x.Lk_ld;
+    const int64_t warps = a.groups[x.P];
+    const int blocks = (int)std::min<int64_t>(cdiv(warps, 8), 148 * 8);
+    if (blocks > 0) sp_unpack1_kernel<<<blocks, 256, 0, st>>>(a);
+    VC_CHECK_LAUNCH();
+    profile_mark(st, "sp_unpack1");
+  }
+  const int g = (int)x.rank;
+  if (x.Lt > 0) {  // text K, V of this head group from the local prompt copy
+    for (int part = 0; part < 2; ++part) {
+      const int64_t n0 = x.pad.fs_base() + (1 + part) * x.pad.SEG + (int64_t)g * x.Hg * x.DP;
+      GemmTcParams gp{};
+      gp.M = x.Lt; gp.N = (int)(x.Hg * x.DP); gp.K = (int)x.D; gp.bias = pp.bias + n0;
+      QkvScatter& s = gp.qkv;
+      s.pad = x.pad; s.D = x.D; s.Lv = x.Lv; s.Lt = x.Lt; s.H = (int)x.Hg; s.head_base = g * (int)x.Hg;
+      s.n_base = n0; s.text_rows = 1; s.sp = sp; s.fs = fs; s.mode = 0;
+      VC_TRY(launch_gemm_tc(xhat + Mr * x.D, x.D, pp.wqkv + n0 * x.D, x.D, gp, EPI_QKV, st));
+    }
+    profile_mark(st, "sp_text_kv_gemm");
+  }
+  const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)x.dh));
+  for (int branch = 0; branch < 2; ++branch) {
+    AttnTcParams a{};
+    a.H = (int)x.Hg; a.dh = (int)x.dh; a.scale_log2 = scale_log2;
+    a.out = (bf*)send2; a.ld_out = 0; a.col_off = 0; a.out_seq_rows = 0;
+    a.spo.P = (int)x.P; a.spo.branch = branch; a.spo.F = (int)x.F; a.spo.Lv = (int)x.Lv; a.spo.Dg = x.Dg;
+    for (int r = 0; r <= x.P; ++r) { a.spo.vb[r] = x.vb[r]; a.spo.base[r] = x.s2_off[r]; }
+    if (branch == 0) {
+      a.Lq = (int)x.Lv; a.Lk = (int)x.Lv; a.n_bias = 0; a.bias_log2 = 0.f;
+      VC_TRY(launch_attn_tc(a, sp.q, sp.k, sp.vt, (int)x.F, x.Lv, x.Lv, x.Lv_ld, (int)x.DP, st));
+      profile_mark(st, "sp_attn_spatial");
+    } else {
+      a.Lq = (int)x.Nv; a.Lk = (int)(x.Lt + x.Nv); a.n_bias = (int)x.Lt; a.bias_log2 = (float)log2((double)x.F);
+      VC_TRY(launch_attn_tc(a, fs.q, fs.k, fs.vt, 1, x.Nv, x.Lt + x.Nv, x.Lk_ld, (int)x.DP, st));
+      profile_mark(st, "sp_attn_fullseq");
+    }
+  }
+  return VC_OK;
+}
+
+int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, const float* x_local,
+                 float* out_local, int add_residual, void* ws, size_t ws_bytes, void* stream) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x));
+  const SpWs w = sp_ws(x);
+  if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  typedef __nv_bfloat16 bf;
+  const PackedPtrs pp = packed_ptrs(x, packed);
+  const int64_t Mr = x.M[x.rank];
+  if (Mr == 0) return VC_OK;
+  bf* acat = (bf*)((char*)ws + w.acat);
+  {
+    const int64_t total = x.P * 2 * Mr * (x.Dg / 2);
+    const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+    sp_unpack2_kernel<<<blocks, 256, 0, st>>>((const bf*)recv2, acat, (int)x.P, Mr, x.Dg, x.D);
+    VC_CHECK_LAUNCH();
+    profile_mark(st, "sp_unpack2");
+  }
+  GemmTcParams g{};
+  g.M = Mr; g.N = (int)x.D; g.K = (int)(3 * x.D);
+  g.out_f32 = out_local; g.ldo = x.D; g.R = add_residual ? x_local : nullptr; g.ldr = x.D;
+  VC_TRY(launch_gemm_tc(acat, 3 * x.D, pp.wo, 3 * x.D, g, EPI_F32, st));
+  profile_mark(st, "sp_oproj_gemm");
+  return VC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,307 @@
+"""Sequence-parallel block forward over one 8xB200 box (the paper's
+memory-efficient hybrid-parallel scheme, spatial shard axis).
+
+Reference: run_sp_iteration stage 3 (executor.py:561-626) with
+_branch_head_parallel (executor.py:332-413): rank r holds visual rows
+[vb[r], vb[r+1]) of every frame; the spatial and full-sequence branches
+exchange q/k/v by head group (all-to-all #1), attend over full sequences for
+H/P heads, and send the output columns back to the row owners (all-to-all
+#2); the temporal branch is rank-local.
+
+The three rank-local stages are CUDA (vc_sp_stage1/2/3 in the C ABI); the
+two all-to-alls are NCCL `all_to_all_single` calls over NVLink/NVSwitch
+issued here through torch.distributed (one process per GPU). An
+`Exchange` object abstracts the collective so the same driver also runs
+(a) a gloo world on CPU in the tests (with numpy stand-ins for the stages)
+and (b) P virtual ranks in one process on one GPU for the parity test.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+# ---------------------------------------------------------------------------
+# Integer shard maps (exact restatements; executor.py:187-245)
+# ---------------------------------------------------------------------------
+
+def contiguous_bounds(n: int, p: int) -> list:
+    """executor.py:187-191: p+1 split points, bounds[i] = i*n//p."""
+    if p < 1:
+        raise ValueError(f"cannot split into {p} parts")
+    return [i * n // p for i in range(p + 1)]
+
+
+def placement_division(text_len: int, visual_len: int, p: int, placement: str = "separate"):
+    """executor.py:216-229 (the 'separate' placement the paper uses; 'fused'
+    is the ablation baseline and is not run on the GPU path)."""
+    if placement == "separate":
+        tb, vb = contiguous_bounds(text_len, p), contiguous_bounds(visual_len, p)
+        return [tb[i + 1] - tb[i] for i in range(p)], [vb[i + 1] - vb[i] for i in range(p)]
+    if placement == "fused":
+        b = contiguous_bounds(text_len + visual_len, p)
+        out = []
+        for lo, hi in zip(b[:-1], b[1:]):
+            t = max(0, min(text_len, hi) - min(text_len, lo))
+            out.append((t, hi - lo - t))
+        return [t for t, _ in out], [v for _, v in out]
+    raise ValueError(f"unknown text placement {placement!r}")
+
+
+def prefix_bounds(counts) -> list:
+    """executor.py:241-245."""
+    out = [0]
+    for c in counts:
+        out.append(out[-1] + c)
+    return out
+
+
+def head_group_columns(dim: int, heads: int, p: int, g: int):
+    """Columns of head group g: [g*D/P, (g+1)*D/P) = heads [g*H/P, (g+1)*H/P)
+    (executor.py:336-337, :372-373)."""
+    if heads % p:
+        raise ValueError(f"head-parallel attention needs sp_size to divide {heads} heads, got {p}")
+    w = dim // p
+    return g * w, (g + 1) * w
+
+
+def check_plan(frames, visual_len, heads, p):
+    """executor.py:517-529 validity."""
+    if p > visual_len:
+        raise ValueError(f"cannot spread {visual_len} visual tokens per frame over {p} devices")
+    if p > 1 and heads % p != 0:
+        raise ValueError(f"head-parallel attention needs sp_size to divide {heads} heads, got {p}")
+
+
+def exchange_counts(frames, visual_len, heads, dim, p, rank, head_pad):
+    """Per-peer element counts of the two all-to-alls (bf16 elements):
+    send1/recv1 carry q,k,v of 2 branches for H/P heads (head dim padded to
+    head_pad); send2/recv2 carry 2 branches' attention outputs (H/P * dh)."""
+    vb = contiguous_bounds(visual_len, p)
+    M = [frames * (vb[r + 1] - vb[r]) for r in range(p)]
+    hg, dg = heads // p, dim // p
+    return {
+        "send1": [6 * M[rank] * hg * head_pad for _ in range(p)],
+        "recv1": [6 * M[r] * hg * head_pad for r in range(p)],
+        "send2": [2 * M[r] * dg for r in range(p)],
+        "recv2": [2 * M[rank] * dg for _ in range(p)],
+    }
+
+
+def head_pad(dh: int) -> int:
+    return 64 if dh <= 64 else 80 if dh <= 80 else 128 if dh <= 128 else 0
+
+
+# ---------------------------------------------------------------------------
+# Collectives
+# ---------------------------------------------------------------------------
+
+class TorchExchange:
+    """all_to_all_single over a torch.distributed group (NCCL on GPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def all_to_all(self, recv, send, recv_counts, send_counts):
+        self.dist.all_to_all_single(recv, send, recv_counts, send_counts, group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# The rank-local CUDA stages
+# ---------------------------------------------------------------------------
+
+class SPBlock:
+    """One rank's share of a sequence-parallel block forward (bf16)."""
+
+    def __init__(self, torch, device_block, frames, visual_len, text_len, nranks, rank):
+        if device_block.dtype != "bf16":
+            raise ValueError("sequence parallelism runs the bf16 path")
+        self.torch = torch
+        self.db = device_block
+        D, H = device_block.dim, device_block.heads
+        check_plan(frames, visual_len, H, nranks)
+        self.plan = _lib.SpPlan(_lib.shape(frames, visual_len, text_len, D, H, "bf16"), nranks, rank)
+        lib = _lib.load()
+        _lib.check(lib.vc_sp_check(C.byref(self.plan)), "sp plan")
+        self.F, self.Lv, self.Lt, self.D, self.H, self.P, self.rank = frames, visual_len, text_len, D, H, nranks, rank
+        vb = (C.c_int32 * (nranks + 1))()
+        _lib.check(lib.vc_sp_bounds(C.byref(self.plan), vb))
+        self.vb = list(vb)
+        self.counts = {k: [int(lib.vc_sp_exchange_elems(C.byref(self.plan), i, r)) for r in range(nranks)]
+                       for i, k in enumerate(("send1", "recv1", "send2", "recv2"))}
+        dev = "cuda"
+        bf = torch.bfloat16
+        self.send1 = torch.empty(sum(self.counts["send1"]), dtype=bf, device=dev)
+        self.recv1 = torch.empty(sum(self.counts["recv1"]), dtype=bf, device=dev)
+        self.send2 = torch.empty(sum(self.counts["send2"]), dtype=bf, device=dev)
+        self.recv2 = torch.empty(sum(self.counts["recv2"]), dtype=bf, device=dev)
+        self.ws_bytes = int(lib.vc_sp_workspace_bytes(C.byref(self.plan)))
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
+
+    @property
+    def local_rows(self):
+        return self.vb[self.rank], self.vb[self.rank + 1]
+
+    def stage1(self, x_local, prompt):
+        lib = _lib.load()
+        _lib.check(lib.vc_sp_stage1(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(x_local),
+                                    _lib.ptr(prompt) if self.Lt else C.c_void_p(0), _lib.ptr(self.send1),
+                                    _lib.ptr(self.ws), self.ws_bytes, _lib.stream_ptr(self.torch)), "sp stage1")
+
+    def stage2(self):
+        lib = _lib.load()
+        _lib.check(lib.vc_sp_stage2(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(self.recv1),
+                                    _lib.ptr(self.send2), _lib.ptr(self.ws), self.ws_bytes,
+                                    _lib.stream_ptr(self.torch)), "sp stage2")
+
+    def stage3(self, x_local, out_local, add_residual=False):
+        lib = _lib.load()
+        _lib.check(lib.vc_sp_stage3(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(self.recv2),
+                                    _lib.ptr(x_local), _lib.ptr(out_local), 1 if add_residual else 0,
+                                    _lib.ptr(self.ws), self.ws_bytes, _lib.stream_ptr(self.torch)), "sp stage3")
+
+    def forward(self, x_local, prompt, out_local, exchange, add_residual=False):
+        """x_local [F, vc_r, D] fp32 -> out_local [F, vc_r, D] fp32 (block
+        output of the local rows, + x_local if add_residual)."""
+        return run_stages(self, x_local, prompt, out_local, exchange, add_residual)
+
+
+def run_stages(stages, x_local, prompt, out_local, exchange, add_residual=False):
+    """The rank-local schedule: stage1 -> a2a #1 -> stage2 -> a2a #2 -> stage3.
+    `stages` provides stage1/2/3, the four exchange buffers and per-peer
+    counts (SPBlock on the GPU; a numpy stand-in in the CPU gloo test)."""
+    stages.stage1(x_local, prompt)
+    exchange.all_to_all(stages.recv1, stages.send1, stages.counts["recv1"], stages.counts["send1"])
+    stages.stage2()
+    exchange.all_to_all(stages.recv2, stages.send2, stages.counts["recv2"], stages.counts["send2"])
+    stages.stage3(x_local, out_local, add_residual)
+    return out_local
+
+
+def emulate_sp_forward(torch, device_block, x, prompt, nranks, add_residual=False):
+    """Run the P-rank algorithm with P virtual ranks in one process on one GPU:
+    stage k of every rank, then the all-to-all as buffer copies. Used by the
+    parity tests (a real multi-GPU run uses SPBlock.forward + TorchExchange;
+    ranks here never wait on one another, so this is safe on one device)."""
+    F, Lv, D = x.shape
+    Lt = prompt.shape[0] if prompt is not None else 0
+    blocks = [SPBlock(torch, device_block, F, Lv, Lt, nranks, r) for r in range(nranks)]
+    xs = [x[:, b.vb[r]:b.vb[r + 1]].contiguous() for r, b in enumerate(blocks)]
+    outs = [torch.empty_like(t) for t in xs]
+
+    def exchange(send_name, recv_name):
+        for g in range(nranks):
+            pieces = []
+            for r in range(nranks):
+                off = sum(blocks[r].counts[send_name][:g])
+                pieces.append(getattr(blocks[r], send_name)[off:off + blocks[r].counts[send_name][g]])
+            recv = getattr(blocks[g], recv_name)
+            torch.cat(pieces, out=recv)
+
+    for r in range(nranks):
+        blocks[r].stage1(xs[r], prompt)
+    exchange("send1", "recv1")
+    for r in range(nranks):
+        blocks[r].stage2()
+    exchange("send2", "recv2")
+    for r in range(nranks):
+        blocks[r].stage3(xs[r], outs[r], add_residual)
+    return torch.cat(outs, dim=1)
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun, one rank per GPU)
+# ---------------------------------------------------------------------------
+
+def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops, load_peaks,
+             ClockSampler, cpu_sample, cpu_cores):
+    import json
+    import torch.distributed as dist
+
+    from .model import DeviceBlock
+    from .numerics import SeededRng
+    from .model import BlockParams
+
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    F, Lv, Lt, D, H, name = CONFIGS[args.config]
+    blk = BlockParams.init(SeededRng(2025).split(1000), D)
+    db = DeviceBlock(torch, blk, H, "bf16")
+    spb = SPBlock(torch, db, F, Lv, Lt, world, rank)
+    lo, hi = spb.local_rows
+    g = torch.Generator(device="cuda").manual_seed(2025)
+    x_full = torch.randn((F, Lv, D), device="cuda", generator=g)  # same on every rank (same seed)
+    prompt = torch.randn((Lt, D), device="cuda", generator=g)
+    x_local = x_full[:, lo:hi].contiguous()
+    del x_full
+    out = torch.empty_like(x_local)
+    ex = TorchExchange()
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        spb.forward(x_local, prompt, out, ex)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            spb.forward(x_local, prompt, out, ex)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms.item())
+    Nv = F * Lv
+    value = Nv / (ms_per_step / 1e3)
+    # end to end: host (pinned) local rows in, host out, per rank
+    xh = x_local.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x_local)
+    for _ in range(2):
+        xd.copy_(xh, non_blocking=True)
+        spb.forward(xd, prompt, out, ex)
+        oh.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        spb.forward(xd, prompt, out, ex)
+        oh.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    flops = sum(algorithmic_flops(F, Lv, Lt, D, H).values())
+    peaks = load_peaks()
+    a2a_bytes = 2 * (sum(spb.counts["send1"]) + sum(spb.counts["send2"]))  # bf16 bytes sent per rank
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (torch.randn inputs, SeededRng random-init 2B-shape weights)",
+            "config": {"workload": name, "frames": F, "visual_len": Lv, "text_len": Lt, "dim": D, "heads": H,
+                       "tokens_per_step": Nv,
+                       "parallelism": f"sequence parallel sp{world} (spatial shard axis, head-parallel a2a, NCCL)",
+                       "l2": "inputs larger than L2 on every rank"},
+            "roofline": {"bound": "tensor", "kernel": "whole block (per GPU)",
+                         "achieved": flops / world / (ms_per_step / 1e3) / 1e12, "peak": peaks["tc_sus"],
+                         "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peaks["tc_sus"],
+                         "traffic": None},
+            "a2a": {"bytes_sent_per_rank_per_step": a2a_bytes},
+            "cpu_baseline": None,
+            "e2e": {"value": Nv / (float(e2e.item()) / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(xh.numel() * 4) * world, "d2h_bytes_per_step": int(oh.numel() * 4) * world},
+            "clocks": clk.summary(),
+            "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
