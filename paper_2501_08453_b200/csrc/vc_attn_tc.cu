@@ -400,9 +400,14 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
   if (p.Lq <= 0 || nseq <= 0) return VC_OK;
   if (p.Lk <= 0) { set_error("attention needs at least one key"); return VC_EINVAL; }
   if (nseq > 65535 || p.H > 65535) { set_error("attention grid too large"); return VC_ENOTSUP; }
+  const bool one_tile = getenv("VC_ATTN_ONE_TILE") != nullptr;  // A/B switch for profiling
   switch (DP) {
-    case 64: return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-    case 80: return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 64:
+      if (!one_tile) return launch_attn_tc2<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 80:
+      if (!one_tile) return launch_attn_tc2<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 128: return launch_dp<128>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
   }
   set_error("tcgen05 attention: unsupported padded head dim %d", DP);
