@@ -20,6 +20,12 @@ namespace {
 using namespace attn;
 
 constexpr int kThreads2 = 384;
+// Fraction of exponentials computed by the FMA-pipe polynomial instead of
+// MUFU.EX2: one pair in kPolyEvery (MUFU is the softmax limiter on B200).
+#ifndef VC_POLY_EVERY
+#define VC_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = VC_POLY_EVERY;
 
 template <int DP>
 struct Cfg2 {
@@ -247,8 +253,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
             if (key + 1 >= p.Lk) x1 = -INFINITY;
           }
           float2 e = ptx::ffma2(make_float2(x0, x1), sc2, nm2);
-          e.x = ptx::ex2(e.x);
-          e.y = ptx::ex2(e.y);
+          if (kPolyEvery > 0 && ((i >> 1) % kPolyEvery) == kPolyEvery - 1) {
+            e = ptx::ex2_poly2(e);  // every kPolyEvery-th pair on the FMA pipe
+          } else {
+            e.x = ptx::ex2(e.x);
+            e.y = ptx::ex2(e.y);
+          }
           if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
           pk[i >> 1] = ptx::bf16x2(e.x, e.y);
         }

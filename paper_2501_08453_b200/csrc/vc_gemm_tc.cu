@@ -29,7 +29,8 @@ constexpr int kThreads = 256;
 
 template <int BN>
 constexpr size_t smem_bytes() {
-  return (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 /*barriers*/ + 1024 /*align*/;
+  return (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 128 /*barriers*/ + 4 * 256 * 4 /*bias*/ +
+         1024 /*align*/;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -52,15 +53,11 @@ __device__ __forceinline__ void qkv_rows(const QkvScatter& s, int b, int64_t m, 
 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m, int n0,
-                                               const uint32_t (&r)[16]) {
+                                               const uint32_t (&r)[16], const float* sbias) {
   if (m >= p.M) return;
   float v[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    v[j] = __uint_as_float(r[j]);
-    const int n = n0 + j;
-    if (p.bias && n < p.N) v[j] += __ldg(p.bias + n);
-  }
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) + (sbias ? sbias[j] : 0.f);  // smem broadcast
   if constexpr (EPI == EPI_F32) {
     float* o = p.out_f32 + m * p.ldo + n0;
     const float* R = p.R ? p.R + m * p.ldr + n0 : nullptr;
@@ -158,13 +155,34 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
   }
 }
 
-template <int BN, int EPI>
+// Rasterised tile order: cluster tiles are walked in groups of kGroupM rows
+// (M) sweeping all N tiles, so the ~148 tiles in flight touch only a few A
+// row-panels and B column-panels and both stay resident in L2.
+constexpr int kGroupM = 4;
+__device__ __forceinline__ void tile_coords(int ct, int num_mc, int num_n, int& mc, int& nt) {
+  const int per_group = kGroupM * num_n;
+  const int g = ct / per_group, r = ct - g * per_group;
+  const int first = g * kGroupM;
+  const int gsize = min(num_mc - first, kGroupM);
+  mc = first + r % gsize;
+  nt = r / gsize;
+}
+
+// CM = CTAs per cluster along M. The CM CTAs of a cluster work on CM
+// consecutive M tiles of the SAME N tile: each loads its own A tile and 1/CM
+// of the B tile, multicast (TMA .multicast::cluster) into every CTA of the
+// cluster, so B crosses L2 once per cluster instead of once per CTA. A stage
+// is refilled only after all CM CTAs' MMAs released it (each MMA commit
+// arrives on the empty barrier of every CTA in the cluster).
+template <int BN, int EPI, int CM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   constexpr uint32_t kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
+  constexpr int kBSlice = BN / CM;  // B rows each CTA loads and multicasts
+  static_assert(kBSlice % 8 == 0, "B slice must keep 8-row swizzle atoms");
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * kABytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * kBBytes);
@@ -175,33 +193,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5;
+  const int rank = CM > 1 ? (int)ptx::cluster_ctarank() : 0;
+  const int cluster = blockIdx.x / CM, nclusters = gridDim.x / CM;
   const int num_m = (int)cdiv(p.M, BM), num_n = (int)cdiv(p.N, BN);
-  const int tiles = num_m * num_n;
+  const int num_mc = (num_m + CM - 1) / CM;  // cluster tiles along M
+  const int ctiles = num_mc * num_n;
   const int kblocks = (int)cdiv(p.K, BK);
 
   if (warp == 0 && ptx::elect_one()) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], CM); }
     for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 128); }
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
   ptx::fence_before_sync();
   __syncthreads();
+  if constexpr (CM > 1) ptx::cluster_sync();  // peers' barriers exist before any multicast
   ptx::fence_after_sync();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (ptx::elect_one()) {
       int s = 0; uint32_t ph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int mt = t % num_m, nt = t / num_m;
+      for (int ct = cluster; ct < ctiles; ct += nclusters) {
+        int mc, nt;
+        tile_coords(ct, num_mc, num_n, mc, nt);
+        const int mt = mc * CM + rank;
         for (int kb = 0; kb < kblocks; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full[s], kABytes + kBBytes);
           ptx::tma_load_2d(sA + s * kABytes, &tmA, &full[s], kb * BK, mt * BM);
-          ptx::tma_load_2d(sB + s * kBBytes, &tmB, &full[s], kb * BK, nt * BN);
+          if constexpr (CM == 1) {
+            ptx::tma_load_2d(sB + s * kBBytes, &tmB, &full[s], kb * BK, nt * BN);
+          } else {
+            ptx::tma_load_2d_mc(sB + s * kBBytes + rank * kBSlice * 128, &tmB, &full[s], kb * BK,
+                                nt * BN + rank * kBSlice, (uint16_t)((1u << CM) - 1));
+          }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -209,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
     int s = 0; uint32_t ph = 0; int local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int ct = cluster; ct < ctiles; ct += nclusters, ++local) {
       const int acc = local & 1;
       ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
       ptx::fence_after_sync();
@@ -226,7 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = ptx::smem_desc(b0 + kk * 32, 0, 1024, ptx::kLayoutSW128);
             ptx::mma_bf16_ss(dtmem, ad, bd, idesc, (kb | kk) != 0);
           }
-          ptx::mma_commit(&empty[s]);
+          if constexpr (CM == 1) ptx::mma_commit(&empty[s]);
+          else ptx::mma_commit_mc(&empty[s], (uint16_t)((1u << CM) - 1));
           if (kb == kblocks - 1) ptx::mma_commit(&tfull[acc]);
         }
         __syncwarp();
@@ -236,10 +266,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
+    float* sbias = reinterpret_cast<float*>(bars + 2 * STAGES + 8) + q * 256;
     int local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int ct = cluster; ct < ctiles; ct += nclusters, ++local) {
       const int acc = local & 1;
-      const int mt = t % num_m, nt = t / num_m;
+      int mc, nt;
+        tile_coords(ct, num_mc, num_n, mc, nt);
+        const int mt = mc * CM + rank;
+      // this tile's bias columns -> a per-warp smem copy (read back as broadcasts)
+      if (p.bias) {
+        __syncwarp();
+        for (int c = lane; c < BN; c += 32) {
+          const int n = nt * BN + c;
+          sbias[c] = n < p.N ? __ldg(p.bias + n) : 0.f;
+        }
+        __syncwarp();
+      }
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::fence_after_sync();
       const int64_t m = (int64_t)mt * BM + q * 32 + lane;
@@ -247,11 +289,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < BN / 16; ++c) {
         const int n0 = nt * BN + c * 16;
-        if (n0 >= p.N) break;
+        if (n0 >= p.N || (int64_t)mt * BM >= p.M) break;
         uint32_t r[16];
         ptx::tmem_ld16(tbase + c * 16, r);
         ptx::tmem_ld_wait();
-        epilogue_chunk<EPI>(p, m, n0, r);
+        epilogue_chunk<EPI>(p, m, n0, r, p.bias ? sbias + c * 16 : nullptr);
       }
       ptx::fence_before_sync();
       ptx::mbar_arrive(&tempty[acc]);
@@ -259,6 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   ptx::fence_before_sync();
   __syncthreads();
+  if constexpr (CM > 1) ptx::cluster_sync();  // no CTA leaves while peers may still signal it
   if (warp == 2) {
     ptx::fence_after_sync();
     ptx::tmem_dealloc(tmem_base, 512);
@@ -289,19 +332,31 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CM>
 int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p,
                 cudaStream_t st) {
   static bool attr_set = false;
   constexpr size_t smem = smem_bytes<BN>();
   if (!attr_set) {
-    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>,
+    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, CM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  const int64_t tiles = cdiv(p.M, BM) * cdiv(p.N, BN);
-  const int grid = (int)std::min<int64_t>(tiles, num_sms());
-  gemm_tc_kernel<BN, EPI><<<grid, kThreads, smem, st>>>(ta, tb, p);
+  const int64_t ctiles = cdiv(cdiv(p.M, BM), CM) * cdiv(p.N, BN);
+  const int clusters = (int)std::min<int64_t>(ctiles, num_sms() / CM);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(clusters * CM));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CM;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, EPI, CM>, ta, tb, p));
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
@@ -367,14 +422,21 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     return VC_EINVAL;
   }
   if (bn == 0) bn = gemm_tc_pick_bn(p.N);
+  // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
+  // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
+  static const bool no_mc = getenv("VC_GEMM_NO_MC") != nullptr;
+  const int cm = (!no_mc && epi != EPI_BF16 && cdiv(p.M, BM) >= 2) ? 2 : 1;
   CUtensorMap ta, tb;
   VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
-  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn, CU_TENSOR_MAP_SWIZZLE_128B));
-#define VC_GEMM_CASE(BNV)                                                  \
-  if (bn == BNV) {                                                         \
-    if (epi == EPI_F32) return launch_impl<BNV, EPI_F32>(ta, tb, p, st);   \
-    if (epi == EPI_BF16) return launch_impl<BNV, EPI_BF16>(ta, tb, p, st); \
-    return launch_impl<BNV, EPI_QKV>(ta, tb, p, st);                       \
+  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn / cm, CU_TENSOR_MAP_SWIZZLE_128B));
+#define VC_GEMM_CASE(BNV)                                                                    \
+  if (bn == BNV) {                                                                           \
+    if (epi == EPI_BF16) return launch_impl<BNV, EPI_BF16, 1>(ta, tb, p, st);                \
+    if (epi == EPI_F32)                                                                      \
+      return cm == 2 ? launch_impl<BNV, EPI_F32, 2>(ta, tb, p, st)                           \
+                     : launch_impl<BNV, EPI_F32, 1>(ta, tb, p, st);                          \
+    return cm == 2 ? launch_impl<BNV, EPI_QKV, 2>(ta, tb, p, st)                             \
+                   : launch_impl<BNV, EPI_QKV, 1>(ta, tb, p, st);                            \
   }
   VC_GEMM_CASE(256)
   VC_GEMM_CASE(240)

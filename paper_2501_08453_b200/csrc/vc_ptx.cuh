@@ -60,6 +60,24 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* m, ui
       "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// Multicast variant: the box lands at the same smem offset in every CTA of
+// ctamask and each destination's mbarrier (same offset) gets complete_tx.
+__device__ __forceinline__ void tma_load_2d_mc(void* smem, const CUtensorMap* m, uint64_t* bar, int x,
+                                               int y, uint16_t ctamask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(ctamask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* m, uint64_t* bar, int x,
                                             int y, int z) {
   asm volatile(
@@ -131,6 +149,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
+// commit arriving on the mbarrier at the same smem offset in every CTA of ctamask
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t ctamask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(ctamask)
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_before_sync() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -195,22 +222,50 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Packed fp32x2 helpers (aliasing-safe packing through mov.b64).
+__device__ __forceinline__ unsigned long long pk2(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ unsigned long long pk2(float a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
 // Packed fp32x2 FMA / add (sm_100 FFMA2 / FADD2: two lanes per instruction).
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&r);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return up2(r);
 }
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return up2(r);
 }
+// 2^x for a pair on the FMA pipe (offloads MUFU): x clamped to >= -126 (2^f can be < 1, keep the biased exponent >= 0),
+// floor via round-down add of 1.5*2^23, degree-3 minimax polynomial for 2^f on
+// [0,1) (max rel err 7.5e-5, below bf16's 3.9e-3), exponent added with LEA.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const unsigned long long xx = pk2(make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f)));
+  unsigned long long t, j, f, q;
+  asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(t) : "l"(xx), "l"(pk2(12582912.f)));
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(j) : "l"(t), "l"(pk2(-12582912.f)));
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(f) : "l"(xx), "l"(j));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(q) : "l"(f), "l"(pk2(0.07802334f)), "l"(pk2(0.22606642f)));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(q) : "l"(q), "l"(f), "l"(pk2(0.69583512f)));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(q) : "l"(q), "l"(f), "l"(pk2(0.99992492f)));
+  const float2 tt = up2(t), qq = up2(q);
+  return make_float2(__uint_as_float(__float_as_uint(qq.x) + (__float_as_uint(tt.x) << 23)),
+                     __uint_as_float(__float_as_uint(qq.y) + (__float_as_uint(tt.y) << 23)));
+}
+
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
