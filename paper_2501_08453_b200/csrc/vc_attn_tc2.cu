@@ -46,7 +46,7 @@ struct Cfg2 {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP>
+template <int DP, int POLY>
 __global__ void __launch_bounds__(kThreads2, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                     const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
             if (key + 1 >= p.Lk) x1 = -INFINITY;
           }
           float2 e = ptx::ffma2(make_float2(x0, x1), sc2, nm2);
-          if (kPolyEvery > 0 && ((i >> 1) % kPolyEvery) == kPolyEvery - 1) {
-            e = ptx::ex2_poly2(e);  // every kPolyEvery-th pair on the FMA pipe
+          if (POLY > 0 && ((i >> 1) % POLY) == POLY - 1) {
+            e = ptx::ex2_poly2(e);  // every POLY-th pair on the FMA pipe
           } else {
             e.x = ptx::ex2(e.x);
             e.y = ptx::ex2(e.y);
@@ -294,15 +294,27 @@ int launch_attn_tc2(const AttnTcParams& p, const void* q, const void* k, const v
   using CF = Cfg2<DP>;
   AttnMaps m;
   VC_TRY(make_attn_maps<DP>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key));
-  static bool attr = false;
-  if (!attr) {
-    VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc2_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
-    attr = true;
-  }
+  static const int poly = getenv("VC_POLY_EVERY") ? atoi(getenv("VC_POLY_EVERY")) : kPolyEvery;
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-  attn_tc2_kernel<DP><<<grid, kThreads2, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);
-  VC_CHECK_LAUNCH();
-  return VC_OK;
+#define VC_ATTN2_CASE(PV)                                                                               \
+  if (poly == PV) {                                                                                     \
+    static bool attr = false;                                                                           \
+    if (!attr) {                                                                                        \
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc2_kernel<DP, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         CF::SMEM));                                                    \
+      attr = true;                                                                                      \
+    }                                                                                                   \
+    attn_tc2_kernel<DP, PV><<<grid, kThreads2, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);    \
+    VC_CHECK_LAUNCH();                                                                                  \
+    return VC_OK;                                                                                       \
+  }
+  VC_ATTN2_CASE(0)
+  VC_ATTN2_CASE(2)
+  VC_ATTN2_CASE(3)
+  VC_ATTN2_CASE(4)
+#undef VC_ATTN2_CASE
+  set_error("VC_POLY_EVERY must be 0, 2, 3 or 4");
+  return VC_EINVAL;
 }
 
 template int launch_attn_tc2<64>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,

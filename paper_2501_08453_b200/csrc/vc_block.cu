@@ -149,8 +149,18 @@ static int block_forward_f32(const Dims& d, const char* packed, const float* x,
   }
   profile_mark(st, "attn_spatial");
   // temporal: sequence l = rows l, l+Lv, ..., l+(F-1)Lv
-  VC_TRY((launch_temporal_attn<float, float>(qkv + 3 * D, ld, D, acat + D, 3 * D, (int)d.F, (int)d.Lv,
-                                             (int)d.H, (int)d.dh, st)));
+  if (d.dh % 2 == 0) {
+    VC_TRY((launch_temporal_attn<float, float>(qkv + 3 * D, ld, D, acat + D, 3 * D, (int)d.F, (int)d.Lv,
+                                               (int)d.H, (int)d.dh, st)));
+  } else {  // odd head dims (tiny test shapes): generic strided kernel
+    AttnArgs<float, float> a{};
+    a.q = qkv + 3 * D; a.ldq = ld; a.q_seq_stride = 1; a.q_tok_stride = d.Lv;
+    a.k = qkv + 4 * D; a.v = qkv + 5 * D; a.ldk = ld; a.k_seq_stride = 1; a.k_tok_stride = d.Lv;
+    a.o = acat + 1 * D; a.ldo = 3 * D; a.o_seq_stride = 1; a.o_tok_stride = d.Lv;
+    a.n_seq = (int)d.Lv; a.len_q = (int)d.F; a.len_k = (int)d.F; a.heads = (int)d.H; a.dh = (int)d.dh;
+    a.scale_log2 = scale_log2;
+    VC_TRY(launch_attn_simt(a, st));
+  }
   profile_mark(st, "attn_temporal");
   // full sequence: queries = all visual rows; keys = Lt text rows (weight F) + all visual rows
   {
