@@ -249,7 +249,7 @@ def run_gpu_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sp:
         return run_gpu_sp(args, torch, world, rank, local)
 
     lib = _lib.load()
@@ -362,6 +362,8 @@ def main():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--sample-frames", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sp", action="store_true",
+                    help="run the sequence-parallel (NCCL) path even at world size 1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -227,6 +227,9 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
     from .numerics import SeededRng
     from .model import BlockParams
 
+    import os
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+        os.environ.setdefault(k, v)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     F, Lv, Lt, D, H, name = CONFIGS[args.config]
     blk = BlockParams.init(SeededRng(2025).split(1000), D)
