@@ -105,6 +105,23 @@ VC_API int vc_block_forward_host(const vc_block_shape* shape, const void* packed
                           float* out_host, void* workspace_dev,
                           size_t workspace_bytes, void* stream);
 
+/* Streamed host path: n block forwards of HOST batches visual_host[i]
+ * ([F][Lv][D] fp32, pinned) sharing one prompt, results to out_host[i].
+ * Double-buffered: the H2D of batch i+1 and the D2H of batch i-1 run on
+ * h2d_stream / d2h_stream while batch i computes on compute_stream, so a
+ * serving loop runs at max(compute, PCIe in, PCIe out) per batch. Work
+ * queued on compute_stream completes after the last copy out. */
+VC_API size_t vc_block_stream_workspace_bytes(const vc_block_shape* shape);
+VC_API int vc_block_forward_host_batched(const vc_block_shape* shape,
+                                         const void* packed_dev, int32_t n,
+                                         const float* const* visual_host,
+                                         const float* prompt_host,
+                                         float* const* out_host,
+                                         void* workspace_dev,
+                                         size_t workspace_bytes,
+                                         void* compute_stream, void* h2d_stream,
+                                         void* d2h_stream);
+
 /* Multi-head attention, numerics.py:87-107: q [sq][D], k/v [sk][D] fp32
  * device, heads contiguous column slices, scale 1/sqrt(D/heads), non-causal.
  * fp32 SIMT path (parity 1e-4 class). */

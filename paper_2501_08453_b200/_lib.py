@@ -42,6 +42,9 @@ SIGNATURES = {
     "vc_block_forward": (C.c_int, [_S, _p, _p, _p, _p, C.c_int, _p, _sz, _p]),
     "vc_block_host_workspace_bytes": (_sz, [_S]),
     "vc_block_forward_host": (C.c_int, [_S, _p, _p, _p, _p, _p, _sz, _p]),
+    "vc_block_stream_workspace_bytes": (_sz, [_S]),
+    "vc_block_forward_host_batched": (C.c_int, [_S, _p, _i32, C.POINTER(C.c_void_p), _p,
+                                                C.POINTER(C.c_void_p), _p, _sz, _p, _p, _p]),
     "vc_attention_f32": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _i32, _i32, _p]),
     "vc_layer_norm_f32": (C.c_int, [_p, _p, _i64, _i32, _p]),
     "vc_embed_frames": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _d, _p]),

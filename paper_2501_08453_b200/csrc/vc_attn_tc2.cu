@@ -46,7 +46,10 @@ struct Cfg2 {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, int POLY>
+// ONES: V's first padding column (d == dh) holds 1.0 (vc_rowops.cu pack), so
+// O[:, dh] accumulates the softmax row sum on the tensor core and the softmax
+// warps skip the sum entirely.
+template <int DP, int POLY, bool ONES>
 __global__ void __launch_bounds__(kThreads2, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                     const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
@@ -259,7 +262,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
             e.x = ptx::ex2(e.x);
             e.y = ptx::ex2(e.y);
           }
-          if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
+          if (!ONES) {
+            if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
+          }
           pk[i >> 1] = ptx::bf16x2(e.x, e.y);
         }
         const uint32_t rowp = sP + h64 * (BQ * 128) + row * 128;
@@ -267,8 +272,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
         for (int u = 0; u < 8; ++u)
           ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       }
-      s2 = ptx::fadd2(s2, s2b);
-      l = l * alpha + (s2.x + s2.y);
+      if (!ONES) {
+        s2 = ptx::fadd2(s2, s2b);
+        l = l * alpha + (s2.x + s2.y);
+      }
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) rescale_o<DP>(tO, alpha);
       ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
       ptx::fence_before_sync();
@@ -276,6 +283,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
     ptx::mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
     ptx::fence_after_sync();
+    if (ONES) {  // row sum accumulated by the tensor core in the ones column
+      uint32_t r1;
+      ptx::tmem_ld1(tO + p.dh, r1);
+      ptx::tmem_ld_wait();
+      l = __uint_as_float(r1);
+    }
     store_out<DP>(p, tO, l, q0 + t * BQ + row, seq, h);
   }
   ptx::fence_before_sync();
@@ -295,25 +308,28 @@ int launch_attn_tc2(const AttnTcParams& p, const void* q, const void* k, const v
   AttnMaps m;
   VC_TRY(make_attn_maps<DP>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key));
   static const int poly = getenv("VC_POLY_EVERY") ? atoi(getenv("VC_POLY_EVERY")) : kPolyEvery;
+  // the ones column exists iff the head dim is padded (V pad column dh = 1.0)
+  static const bool no_ones = getenv("VC_NO_ONES_COLUMN") != nullptr;
+  const bool ones = !no_ones && p.dh < DP;
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-#define VC_ATTN2_CASE(PV)                                                                               \
-  if (poly == PV) {                                                                                     \
-    static bool attr = false;                                                                           \
-    if (!attr) {                                                                                        \
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc2_kernel<DP, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         CF::SMEM));                                                    \
-      attr = true;                                                                                      \
-    }                                                                                                   \
-    attn_tc2_kernel<DP, PV><<<grid, kThreads2, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);    \
-    VC_CHECK_LAUNCH();                                                                                  \
-    return VC_OK;                                                                                       \
+#define VC_ATTN2_CASE(PV, ON)                                                                              \
+  if (poly == PV && ones == ON) {                                                                          \
+    static bool attr = false;                                                                              \
+    if (!attr) {                                                                                           \
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc2_kernel<DP, PV, ON>,                                      \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));          \
+      attr = true;                                                                                         \
+    }                                                                                                      \
+    attn_tc2_kernel<DP, PV, ON><<<grid, kThreads2, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);   \
+    VC_CHECK_LAUNCH();                                                                                     \
+    return VC_OK;                                                                                          \
   }
-  VC_ATTN2_CASE(0)
-  VC_ATTN2_CASE(2)
-  VC_ATTN2_CASE(3)
-  VC_ATTN2_CASE(4)
+  VC_ATTN2_CASE(0, false)
+  VC_ATTN2_CASE(0, true)
+  VC_ATTN2_CASE(4, false)
+  VC_ATTN2_CASE(4, true)
 #undef VC_ATTN2_CASE
-  set_error("VC_POLY_EVERY must be 0, 2, 3 or 4");
+  set_error("VC_POLY_EVERY must be 0 or 4");
   return VC_EINVAL;
 }
 

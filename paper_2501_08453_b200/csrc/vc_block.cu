@@ -290,6 +290,66 @@ int vc_block_forward_host(const vc_block_shape* shape, const void* packed_dev,
   return VC_OK;
 }
 
+size_t vc_block_stream_workspace_bytes(const vc_block_shape* shape) {
+  Dims d;
+  if (check_shape(shape, &d) != VC_OK) return 0;
+  return align_up(workspace_bytes(d), 1024) + 4 * align_up((size_t)d.Nv * d.D * 4, 1024) +
+         align_up((size_t)(d.Lt > 0 ? d.Lt : 1) * d.D * 4, 1024);
+}
+
+int vc_block_forward_host_batched(const vc_block_shape* shape, const void* packed_dev, int32_t n,
+                                  const float* const* visual_host, const float* prompt_host,
+                                  float* const* out_host, void* workspace_dev, size_t workspace_bytes_,
+                                  void* compute_stream, void* h2d_stream, void* d2h_stream) {
+  Dims d;
+  VC_TRY(check_shape(shape, &d));
+  if (n < 0 || (n > 0 && (!visual_host || !out_host))) { set_error("bad batch arguments"); return VC_EINVAL; }
+  if (workspace_bytes_ < vc_block_stream_workspace_bytes(shape)) {
+    set_error("workspace too small for the streamed host path");
+    return VC_EINVAL;
+  }
+  cudaStream_t sc = (cudaStream_t)compute_stream, si = (cudaStream_t)h2d_stream, so = (cudaStream_t)d2h_stream;
+  const size_t xbytes = (size_t)d.Nv * d.D * 4;
+  char* ws = (char*)workspace_dev;
+  size_t off = align_up(workspace_bytes(d), 1024);
+  float* xin[2];
+  float* yout[2];
+  for (int b = 0; b < 2; ++b) { xin[b] = (float*)(ws + off); off += align_up(xbytes, 1024); }
+  for (int b = 0; b < 2; ++b) { yout[b] = (float*)(ws + off); off += align_up(xbytes, 1024); }
+  float* pin = (float*)(ws + off);
+  // events: inputs landed / compute done / result copied out, per staging buffer
+  cudaEvent_t ev[7];
+  for (int i = 0; i < 7; ++i) VC_CHECK_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  cudaEvent_t *in_ready = ev, *done = ev + 2, *out_free = ev + 4, start = ev[6];
+  int rc = VC_OK;
+  // the copy streams start after everything already queued on the compute stream
+  cudaEventRecord(start, sc);
+  cudaStreamWaitEvent(si, start, 0);
+  cudaStreamWaitEvent(so, start, 0);
+  if (d.Lt > 0) cudaMemcpyAsync(pin, prompt_host, (size_t)d.Lt * d.D * 4, cudaMemcpyHostToDevice, sc);
+  for (int i = 0; i < n && rc == VC_OK; ++i) {
+    const int b = i & 1;
+    // H2D of batch i may overwrite xin[b] once batch i-2's compute has read it
+    if (i >= 2) cudaStreamWaitEvent(si, done[b], 0);
+    cudaMemcpyAsync(xin[b], visual_host[i], xbytes, cudaMemcpyHostToDevice, si);
+    cudaEventRecord(in_ready[b], si);
+    cudaStreamWaitEvent(sc, in_ready[b], 0);
+    if (i >= 2) cudaStreamWaitEvent(sc, out_free[b], 0);  // D2H of batch i-2 done with yout[b]
+    rc = vc_block_forward(shape, packed_dev, xin[b], pin, yout[b], 0, workspace_dev, workspace_bytes(d), sc);
+    cudaEventRecord(done[b], sc);
+    cudaStreamWaitEvent(so, done[b], 0);
+    cudaMemcpyAsync(out_host[i], yout[b], xbytes, cudaMemcpyDeviceToHost, so);
+    cudaEventRecord(out_free[b], so);
+  }
+  // join: the compute stream completes after the last copy out
+  cudaEventRecord(start, so);
+  cudaStreamWaitEvent(sc, start, 0);
+  for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);  // deferred until the events complete
+  if (rc != VC_OK) return rc;
+  VC_CHECK_CUDA(cudaGetLastError());
+  return VC_OK;
+}
+
 int vc_attention_f32(const float* q, const float* k, const float* v, float* out, int32_t sq,
                      int32_t sk, int32_t dim, int32_t heads, void* stream) {
   if (heads < 1 || dim % heads != 0) {

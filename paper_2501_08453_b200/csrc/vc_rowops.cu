@@ -201,9 +201,21 @@ __device__ __forceinline__ bool qkv_source(int64_t n, int D, int H, bool padded,
     return true;
   } else { b = 2; const int64_t r = n - q.fs_base(); which = (int)(r / q.SEG); j = r % q.SEG; }
   const int h = (int)(j / q.DP), d = (int)(j % q.DP);
-  if (h >= H || d >= dh) return false;
+  if (h >= H || d >= dh) {
+    c = (h < H && d == dh) ? -1 : -2;  // -1: first V pad column (the ones column, see below)
+    return false;
+  }
   c = h * dh + d;
   return true;
+}
+
+// The first padding column of every head's V (d == dh < DP) is a constant 1.0
+// (zero weights, bias 1): the P.V MMA then accumulates the softmax row sum
+// in O[:, dh] for free, in the same bf16 P the numerator uses.
+__device__ __forceinline__ bool is_ones_column(int64_t n, int D, int H, QkvPad q) {
+  int b, which, c;
+  if (qkv_source(n, D, H, true, q, b, which, c)) return false;
+  return b != 1 && which == 2 && c == -1;
 }
 
 template <typename T, bool KMAJOR>
@@ -229,7 +241,10 @@ __global__ void pack_bias_kernel(const float* __restrict__ raw, float* __restric
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   int b, which, c;
-  if (!qkv_source(n, D, H, padded, q, b, which, c)) { bias[n] = 0.f; return; }
+  if (!qkv_source(n, D, H, padded, q, b, which, c)) {
+    bias[n] = (padded && is_ones_column(n, D, H, q)) ? 1.f : 0.f;
+    return;
+  }
   const float* beta = raw_branch(raw, b, D) + D;
   const float* W = raw_w(raw, b, which, D);
   double acc = 0.0;

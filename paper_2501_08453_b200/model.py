@@ -232,6 +232,40 @@ def parallel_block_forward(block: BlockParams, visual, text, heads: int, *, dtyp
     return out.double().cpu().numpy() if as_numpy else out
 
 
+def block_forward_host_stream(block: BlockParams, visuals, prompt, heads: int, outs=None, *, dtype=None):
+    """Serving path: parallel_block_forward over a list of HOST batches (pinned
+    float32 torch tensors [F, Lv, D]) with one shared prompt [Lt, D], through
+    vc_block_forward_host_batched: H2D of batch i+1 and D2H of batch i-1
+    overlap the compute of batch i. Returns the list of host outputs."""
+    torch = _lib.require_cuda()
+    dtype = _resolve_dtype(dtype)
+    F, Lv, D = visuals[0].shape
+    Lt = prompt.shape[0]
+    db = device_block(torch, block, heads, dtype)
+    lib = _lib.load()
+    shp = _lib.shape(F, Lv, Lt, D, heads, dtype)
+    nbytes = lib.vc_block_stream_workspace_bytes(C.byref(shp))
+    if nbytes == 0:
+        _lib.check(lib.vc_block_shape_check(C.byref(shp)), "shape")
+    ws = workspace(torch, nbytes)
+    if outs is None:
+        outs = [torch.empty((F, Lv, D), dtype=torch.float32).pin_memory() for _ in visuals]
+    pin = prompt if _is_torch(prompt) else torch.from_numpy(np.ascontiguousarray(prompt, dtype=np.float32))
+    pin = pin.contiguous().pin_memory() if not pin.is_pinned() else pin
+    n = len(visuals)
+    xs = (C.c_void_p * n)(*[v.data_ptr() for v in visuals])
+    ys = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    streams = _HOST_STREAMS.setdefault("s", (torch.cuda.Stream(), torch.cuda.Stream()))
+    _lib.check(lib.vc_block_forward_host_batched(C.byref(shp), _lib.ptr(db.packed), n, xs,
+                                                 C.c_void_p(pin.data_ptr()), ys, _lib.ptr(ws), ws.numel(),
+                                                 _lib.stream_ptr(torch), C.c_void_p(streams[0].cuda_stream),
+                                                 C.c_void_p(streams[1].cuda_stream)), "host stream")
+    return outs
+
+
+_HOST_STREAMS: dict = {}
+
+
 def _single_branch(params, slot, visual, text, heads, dtype):
     dim = visual.shape[2]
     z = BranchParams.zeros(dim)

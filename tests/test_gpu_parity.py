@@ -199,3 +199,20 @@ def test_config2_full_bf16_vs_fp32_transitive(vc):
     y16 = vc.parallel_block_forward(blk, xt, text, H, dtype="bf16").double().cpu().numpy()
     assert np.isfinite(y16).all()
     assert rel_l2(y16, y32) <= BF16_TOL
+
+
+def test_host_stream_matches_device_forward(vc):
+    # serving path (vc_block_forward_host_batched): each batch equals the
+    # single device-resident forward of the same input
+    import torch
+    from paper_2501_08453_b200.model import block_forward_host_stream
+    F, Lv, Lt, D, H = 3, 64, 32, 256, 8
+    blk, x, prompt = block_case(vc, "stream", F, Lv, Lt, D)
+    xs = [torch.from_numpy((x * (i + 1)).astype(np.float32)).pin_memory() for i in range(5)]
+    pt = torch.from_numpy(prompt.astype(np.float32)).pin_memory()
+    for dt in ("fp32", "bf16"):
+        outs = block_forward_host_stream(blk, xs, pt, H, dtype=dt)
+        torch.cuda.synchronize()
+        for i in range(5):
+            ref = vc.parallel_block_forward(blk, x * (i + 1), vc.anchor_text(prompt, F), H, dtype=dt)
+            assert np.array_equal(outs[i].double().numpy(), ref), (dt, i)
