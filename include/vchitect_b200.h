@@ -143,6 +143,16 @@ VC_API int vc_embed_frames(const float* latents_dev, const float* w_in_dev,
                     int32_t h, int32_t w, int32_t c, int32_t patch,
                     int32_t dim, double t, void* stream);
 
+/* Row subset of vc_embed_frames: tokens [tok0, tok0+ntok) of every frame ->
+ * x [F][ntok][D]. A sequence-parallel rank embeds its own rows directly
+ * (the embedding is position-wise), replacing the reference's frame-wise
+ * embed + all-to-all reshard (executor.py:535-559) with no communication. */
+VC_API int vc_embed_frames_rows(const float* latents_dev, const float* w_in_dev,
+                                float* x_dev, int32_t frames, int32_t first_frame,
+                                int32_t tok0, int32_t ntok, int32_t h, int32_t w,
+                                int32_t c, int32_t patch, int32_t dim, double t,
+                                void* stream);
+
 /* ToyDenoiser.forward's output projection + unpatchify crop,
  * model.py:331-333 + model.py:67-76: x [F][Lv][D], w_out [D][p*p*c] ->
  * eps [F][h][w][c] fp32. */

@@ -328,8 +328,10 @@ int launch_attn_tc2(const AttnTcParams& p, const void* q, const void* k, const v
   VC_ATTN2_CASE(0, true)
   VC_ATTN2_CASE(4, false)
   VC_ATTN2_CASE(4, true)
+  VC_ATTN2_CASE(2, true)
+  VC_ATTN2_CASE(3, true)
 #undef VC_ATTN2_CASE
-  set_error("VC_POLY_EVERY must be 0 or 4");
+  set_error("VC_POLY_EVERY must be 0 or 4 (2, 3 with the ones column)");
   return VC_EINVAL;
 }
 

@@ -376,7 +376,15 @@ int vc_embed_frames(const float* lat, const float* w_in, float* x, int32_t F, in
                     void* stream) {
   if (dim % 2 != 0) { set_error("embedding dim must be even, got %d", dim); return VC_EINVAL; }
   if (F < 1 || h < 1 || w < 1 || c < 1 || patch < 1) { set_error("bad latent shape"); return VC_EINVAL; }
-  return launch_embed(lat, w_in, x, F, first_frame, h, w, c, patch, dim, t, (cudaStream_t)stream);
+  return launch_embed(lat, w_in, x, F, first_frame, 0, -1, h, w, c, patch, dim, t, (cudaStream_t)stream);
+}
+
+int vc_embed_frames_rows(const float* lat, const float* w_in, float* x, int32_t F, int32_t first_frame,
+                         int32_t tok0, int32_t ntok, int32_t h, int32_t w, int32_t c, int32_t patch,
+                         int32_t dim, double t, void* stream) {
+  if (dim % 2 != 0) { set_error("embedding dim must be even, got %d", dim); return VC_EINVAL; }
+  if (F < 1 || h < 1 || w < 1 || c < 1 || patch < 1 || ntok < 0) { set_error("bad latent shape"); return VC_EINVAL; }
+  return launch_embed(lat, w_in, x, F, first_frame, tok0, ntok, h, w, c, patch, dim, t, (cudaStream_t)stream);
 }
 
 int vc_unembed_frames(const float* x, const float* w_out, float* eps, int32_t F, int32_t h,

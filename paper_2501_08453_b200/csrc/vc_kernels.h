@@ -27,8 +27,8 @@ template <typename OutT>
 int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
                    cudaStream_t st);
 
-int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int h, int w,
-                 int c, int p, int D, double t, cudaStream_t st);
+int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int tok0,
+                 int ntok, int h, int w, int c, int p, int D, double t, cudaStream_t st);
 int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h, int w, int c,
                    int p, int D, cudaStream_t st);
 // Column space of the bf16 QKV GEMM: the spatial / full-sequence Q, K, V

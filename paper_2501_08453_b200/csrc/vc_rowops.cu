@@ -82,16 +82,19 @@ __device__ __forceinline__ double sinus(double pos, int d, int D) {
 }
 
 __global__ void embed_kernel(const float* __restrict__ lat, const float* __restrict__ w_in,
-                             float* __restrict__ x, int F, int first_frame, int h, int w, int c,
-                             int p, int D, double t) {
+                             float* __restrict__ x, int F, int first_frame, int tok0, int ntok, int h,
+                             int w, int c, int p, int D, double t) {
+  // x[f][k][d] for tokens i = tok0 + k of each frame (a sequence-parallel rank
+  // embeds only its own rows; model.py:303-314 is position-wise, so the rows
+  // equal the single-device ones exactly)
   const int gh = (h + p - 1) / p, gw = (w + p - 1) / p;
   const int Lv = gh * gw, pd = p * p * c;
-  const int64_t total = (int64_t)F * Lv * D;
+  const int64_t total = (int64_t)F * ntok * D;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int d = (int)(e % D);
-    const int64_t tok = e / D;  // f*Lv + i
-    const int f = (int)(tok / Lv), i = (int)(tok % Lv);
+    const int64_t r = e / D;  // f*ntok + k
+    const int f = (int)(r / ntok), i = tok0 + (int)(r % ntok);
     const int gy = i / gw, gx = i % gw;
     double acc = 0.0;
     for (int j = 0; j < pd; ++j) {
@@ -100,7 +103,7 @@ __global__ void embed_kernel(const float* __restrict__ lat, const float* __restr
       if (yy < h && xx < w)
         acc += (double)lat[(((int64_t)f * h + yy) * w + xx) * c + ch] * (double)w_in[(int64_t)j * D + d];
     }
-    acc += sinus((double)(tok + (int64_t)first_frame * Lv), d, D);
+    acc += sinus((double)((int64_t)(first_frame + f) * Lv + i), d, D);
     acc += sinus(t, d, D);
     x[e] = (float)acc;
   }
@@ -140,12 +143,15 @@ __global__ void unembed_kernel(const float* __restrict__ x, const float* __restr
   }
 }
 
-int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int h, int w,
-                 int c, int p, int D, double t, cudaStream_t st) {
-  const int64_t total = (int64_t)F * ((h + p - 1) / p) * ((w + p - 1) / p) * D;
+int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int tok0,
+                 int ntok, int h, int w, int c, int p, int D, double t, cudaStream_t st) {
+  const int Lv = ((h + p - 1) / p) * ((w + p - 1) / p);
+  if (ntok < 0) ntok = Lv - tok0;
+  if (tok0 < 0 || tok0 + ntok > Lv) { set_error("token range [%d, %d) outside %d tokens", tok0, tok0 + ntok, Lv); return VC_EINVAL; }
+  const int64_t total = (int64_t)F * ntok * D;
   if (total <= 0) return VC_OK;
   const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
-  embed_kernel<<<blocks, 256, 0, st>>>(lat, w_in, x, F, first_frame, h, w, c, p, D, t);
+  embed_kernel<<<blocks, 256, 0, st>>>(lat, w_in, x, F, first_frame, tok0, ntok, h, w, c, p, D, t);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
