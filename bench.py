@@ -251,6 +251,8 @@ def run_gpu_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if args.config == 3:
+        return run_model_step(args, torch, world, rank, local)
     if world > 1 or args.sp:
         return run_gpu_sp(args, torch, world, rank, local)
 
@@ -361,6 +363,74 @@ def run_gpu_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def run_model_step(args, torch, world, rank, local):
+    """Config 3: one full 2B-model denoise step (ToyDenoiser.forward: embed +
+    40 blocks + unembed, model.py:327-333) on a 480p 40-frame latent clip;
+    sequence-parallel over the ranks when world > 1 (sp.sp_model_forward)."""
+    import paper_2501_08453_b200 as vc
+    from paper_2501_08453_b200 import sp
+    F, h, w, Lt, D, H, depth = 40, 60, 90, 256, 1584, 24, args.depth
+    name = f"config3 2B ToyDenoiser step ({depth} blocks, 40 frames x 60x90 latents -> 30x45 patches, 256 text)"
+    Lv = (h // 2) * (w // 2)
+    Nv = F * Lv
+    model = vc.ToyDenoiser.init(vc.SeededRng(2025), vc.PatchSpec(8, 2, 4), D, H, depth)
+    g = torch.Generator(device="cuda").manual_seed(2025)
+    lat = torch.randn((F, h, w, 4), device="cuda", generator=g)
+    prompt = torch.randn((Lt, D), device="cuda", generator=g)
+    stream = torch.cuda.current_stream()
+    if world > 1 or args.sp:
+        import torch.distributed as dist
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29541"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        cache, ex = {}, sp.TorchExchange()
+
+        def step():
+            return sp.sp_model_forward(torch, model, lat, 37, prompt, cache, ex, rank, world)
+        par = f"sequence parallel sp{world} (own-row embed, head-parallel a2a per block, final all-gather)"
+    else:
+        def step():
+            return model.forward(lat, 37, prompt, dtype="bf16")
+        par = "single GPU"
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1 or args.sp:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            eps = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    if world > 1 or args.sp:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms.item())
+    assert torch.isfinite(eps).all().item()
+    flops = depth * sum(algorithmic_flops(F, Lv, Lt, D, H).values())
+    peaks = load_peaks()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": Nv / (ms_per_step / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic latents/prompt, SeededRng random-init 2B weights",
+            "config": {"workload": name, "frames": F, "visual_len": Lv, "text_len": Lt, "dim": D, "heads": H,
+                       "depth": depth, "tokens_per_step": Nv, "parallelism": par},
+            "roofline": {"bound": "tensor", "kernel": "whole model step (per GPU)",
+                         "achieved": flops / world / (ms_per_step / 1e3) / 1e12, "peak": peaks["tc_sus"],
+                         "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peaks["tc_sus"],
+                         "traffic": None},
+            "cpu_baseline": None, "e2e": None, "clocks": clk.summary(), "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1 or args.sp:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_gpu_sp(args, torch, world, rank, local):
     from paper_2501_08453_b200 import sp
     return sp.bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops,
@@ -373,7 +443,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS) + [3])
+    ap.add_argument("--depth", type=int, default=40, help="blocks in the config-3 model step")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--sample-frames", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")

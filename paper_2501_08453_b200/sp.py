@@ -183,35 +183,142 @@ def run_stages(stages, x_local, prompt, out_local, exchange, add_residual=False)
     return out_local
 
 
+class EmulatedRanks:
+    """P virtual ranks in one process on one GPU: stage k of every rank, then
+    the all-to-all as buffer copies with the product's per-peer counts. Used by
+    the parity tests (a real multi-GPU run uses SPBlock.forward with
+    TorchExchange; ranks here never wait on one another, so this is safe on
+    one device)."""
+
+    def __init__(self, torch, device_block, frames, visual_len, text_len, nranks):
+        self.torch = torch
+        self.P = nranks
+        self.blocks = [SPBlock(torch, device_block, frames, visual_len, text_len, nranks, r)
+                       for r in range(nranks)]
+        self.vb = self.blocks[0].vb
+
+    def _exchange(self, send_name, recv_name):
+        for g in range(self.P):
+            pieces = []
+            for r in range(self.P):
+                b = self.blocks[r]
+                off = sum(b.counts[send_name][:g])
+                pieces.append(getattr(b, send_name)[off:off + b.counts[send_name][g]])
+            self.torch.cat(pieces, out=getattr(self.blocks[g], recv_name))
+
+    def block_forward(self, xs, prompt, outs, add_residual=False, device_block=None):
+        """xs / outs: per-rank [F, vc_r, D] fp32 (outs may alias xs)."""
+        for b in self.blocks:
+            if device_block is not None:
+                b.db = device_block
+        for r, b in enumerate(self.blocks):
+            b.stage1(xs[r], prompt)
+        self._exchange("send1", "recv1")
+        for b in self.blocks:
+            b.stage2()
+        self._exchange("send2", "recv2")
+        for r, b in enumerate(self.blocks):
+            b.stage3(xs[r], outs[r], add_residual)
+        return outs
+
+    def split(self, x):
+        return [x[:, self.vb[r]:self.vb[r + 1]].contiguous() for r in range(self.P)]
+
+
 def emulate_sp_forward(torch, device_block, x, prompt, nranks, add_residual=False):
-    """Run the P-rank algorithm with P virtual ranks in one process on one GPU:
-    stage k of every rank, then the all-to-all as buffer copies. Used by the
-    parity tests (a real multi-GPU run uses SPBlock.forward + TorchExchange;
-    ranks here never wait on one another, so this is safe on one device)."""
+    """One SP block forward over P virtual ranks; returns the gathered [F, Lv, D]."""
     F, Lv, D = x.shape
     Lt = prompt.shape[0] if prompt is not None else 0
-    blocks = [SPBlock(torch, device_block, F, Lv, Lt, nranks, r) for r in range(nranks)]
-    xs = [x[:, b.vb[r]:b.vb[r + 1]].contiguous() for r, b in enumerate(blocks)]
+    em = EmulatedRanks(torch, device_block, F, Lv, Lt, nranks)
+    xs = em.split(x)
     outs = [torch.empty_like(t) for t in xs]
-
-    def exchange(send_name, recv_name):
-        for g in range(nranks):
-            pieces = []
-            for r in range(nranks):
-                off = sum(blocks[r].counts[send_name][:g])
-                pieces.append(getattr(blocks[r], send_name)[off:off + blocks[r].counts[send_name][g]])
-            recv = getattr(blocks[g], recv_name)
-            torch.cat(pieces, out=recv)
-
-    for r in range(nranks):
-        blocks[r].stage1(xs[r], prompt)
-    exchange("send1", "recv1")
-    for r in range(nranks):
-        blocks[r].stage2()
-    exchange("send2", "recv2")
-    for r in range(nranks):
-        blocks[r].stage3(xs[r], outs[r], add_residual)
+    em.block_forward(xs, prompt, outs, add_residual)
     return torch.cat(outs, dim=1)
+
+
+# ---------------------------------------------------------------------------
+# Sequence-parallel model step (SURVEY 8(f1)): ToyDenoiser.forward over P ranks
+# ---------------------------------------------------------------------------
+
+def embed_rows(torch, model, lat_dev, t, tok0, ntok):
+    """Rows [tok0, tok0+ntok) of every frame of ToyDenoiser.embed_frame
+    (model.py:303-314) -> [F, ntok, D] fp32. Position-wise, so a rank embeds
+    exactly its own rows: no frame-wise encode + all-to-all reshard
+    (executor.py:535-559) is needed."""
+    from .numerics import to_device_f32
+    F, h, w, c = lat_dev.shape
+    x = torch.empty((F, ntok, model.dim), dtype=torch.float32, device="cuda")
+    w_in = to_device_f32(torch, model.w_in)
+    lib = _lib.load()
+    _lib.check(lib.vc_embed_frames_rows(_lib.ptr(lat_dev), _lib.ptr(w_in), _lib.ptr(x), F, 0, tok0, ntok, h, w, c,
+                                        model.spec.patch, model.dim, float(t), _lib.stream_ptr(torch)), "embed rows")
+    return x
+
+
+def unembed(torch, model, x_full, h, w, c):
+    """ToyDenoiser.forward's output projection + crop (model.py:331-333)."""
+    from .numerics import to_device_f32
+    F = x_full.shape[0]
+    eps = torch.empty((F, h, w, c), dtype=torch.float32, device="cuda")
+    w_out = to_device_f32(torch, model.w_out)
+    lib = _lib.load()
+    _lib.check(lib.vc_unembed_frames(_lib.ptr(x_full), _lib.ptr(w_out), _lib.ptr(eps), F, h, w, c,
+                                     model.spec.patch, model.dim, _lib.stream_ptr(torch)), "unembed")
+    return eps
+
+
+def emulate_sp_model_forward(torch, model, latents, t, prompt, nranks):
+    """ToyDenoiser.forward (bf16) over P virtual ranks: each rank embeds its
+    rows, the blocks run sequence-parallel with the residual fused, the final
+    all-gather (executor.py:683-693) becomes a concatenation, and the
+    replicated unembed runs once."""
+    from .model import device_block
+    from .numerics import to_device_f32
+    lat = to_device_f32(torch, latents)
+    pr = to_device_f32(torch, prompt)
+    F, h, w, c = lat.shape
+    p = model.spec.patch
+    Lv = -(-h // p) * -(-w // p)
+    dbs = [device_block(torch, b, model.heads, "bf16") for b in model.blocks]
+    em = EmulatedRanks(torch, dbs[0], F, Lv, pr.shape[0], nranks)
+    xs = [embed_rows(torch, model, lat, t, em.vb[r], em.vb[r + 1] - em.vb[r]) for r in range(nranks)]
+    for db in dbs:
+        em.block_forward(xs, pr, xs, add_residual=True, device_block=db)
+    return unembed(torch, model, torch.cat(xs, dim=1).contiguous(), h, w, c)
+
+
+def sp_model_forward(torch, model, latents, t, prompt, spb_cache, exchange, rank, nranks, group=None):
+    """ToyDenoiser.forward on this rank of a P-rank job (torchrun + NCCL):
+    embed own rows -> depth x SPBlock.forward (residual fused, in place) ->
+    all-gather the rows (executor.py:683-693) -> unembed. Every rank returns
+    the full eps [F, h, w, c] (the reference's replicated output head)."""
+    import torch.distributed as dist
+
+    from .model import device_block
+    from .numerics import to_device_f32
+    lat = to_device_f32(torch, latents)
+    pr = to_device_f32(torch, prompt)
+    F, h, w, c = lat.shape
+    p = model.spec.patch
+    Lv = -(-h // p) * -(-w // p)
+    dbs = [device_block(torch, b, model.heads, "bf16") for b in model.blocks]
+    key = (F, Lv, pr.shape[0], nranks, rank)
+    if key not in spb_cache:
+        spb_cache[key] = SPBlock(torch, dbs[0], F, Lv, pr.shape[0], nranks, rank)
+    spb = spb_cache[key]
+    lo, hi = spb.local_rows
+    x = embed_rows(torch, model, lat, t, lo, hi - lo)
+    for db in dbs:
+        spb.db = db
+        spb.forward(x, pr, x, exchange, add_residual=True)
+    # all-gather the rows (uneven shards: pad to the largest, gather, trim)
+    vmax = max(spb.vb[r + 1] - spb.vb[r] for r in range(nranks))
+    pad = torch.zeros((F, vmax, model.dim), dtype=torch.float32, device="cuda")
+    pad[:, :hi - lo] = x
+    allx = torch.empty((nranks, F, vmax, model.dim), dtype=torch.float32, device="cuda")
+    dist.all_gather_into_tensor(allx, pad, group=group)
+    full = torch.cat([allx[r, :, :spb.vb[r + 1] - spb.vb[r]] for r in range(nranks)], dim=1).contiguous()
+    return unembed(torch, model, full, h, w, c)
 
 
 # ---------------------------------------------------------------------------

@@ -64,3 +64,25 @@ def test_sp_rejects_bad_plans(torch):
         sp.SPBlock(torch, db, 2, 16, 4, 4, 0)
     with pytest.raises(ValueError, match="cannot spread"):
         sp.SPBlock(torch, db, 2, 3, 4, 6, 0)
+
+
+def test_sp_model_forward_matches_single_gpu(torch):
+    # the sequence-parallel model step (own-row embed, SP blocks
+    # with the residual fused, final gather, replicated unembed) equals the
+    # single-GPU ToyDenoiser.forward and the oracle
+    import paper_2501_08453_b200 as vc
+    from paper_2501_08453_b200 import sp
+    seed, F, h, w, Lt, D, H, depth, t = 2501, 3, 24, 20, 16, 256, 8, 2, 37
+    model = vc.ToyDenoiser.init(vc.SeededRng(seed), vc.PatchSpec(8, 2, 4), D, H, depth)
+    data = vc.SeededRng(seed).split(1 << 20)
+    lat = data.split(1).normal((F, h, w, 4))
+    prompt = data.split(2).normal((Lt, D))
+    single = model.forward(lat, t, prompt, dtype="bf16")
+    om = O.ToyDenoiser(O.PatchSpec(8, 2, 4), D, H, model.w_in, model.w_out,
+                       [O.BlockParams(*[O.BranchParams(*br.arrays()) for br in b.branches()]) for b in model.blocks])
+    ref = om.forward(lat, t, prompt)
+    assert rel_l2(single, ref) <= 2e-2
+    for P in (2, 4):
+        got = sp.emulate_sp_model_forward(torch, model, lat, t, prompt, P).double().cpu().numpy()
+        assert rel_l2(got, single) <= 1e-3, P
+        assert rel_l2(got, ref) <= 2e-2, P
