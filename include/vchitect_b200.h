@@ -160,6 +160,20 @@ VC_API int vc_unembed_frames(const float* x_dev, const float* w_out_dev,
                       float* eps_dev, int32_t frames, int32_t h, int32_t w,
                       int32_t c, int32_t patch, int32_t dim, void* stream);
 
+/* One denoise step, output side: the unembed of vc_unembed_frames with the
+ * DDPM ancestral step reverse_step (diffusion.py:95-116) fused into its
+ * epilogue: x_prev = (x_t - coef_eps * eps) * inv_sqrt_alpha
+ * (+ sqrt_beta * noise when noise != NULL), coef_eps = beta_t /
+ * sqrt(1 - alpha_bar_t), inv_sqrt_alpha = 1 / sqrt(alpha_t) (host fp64 from
+ * the schedule). eps may be NULL (not stored). All [F][h][w][c] fp32. */
+VC_API int vc_unembed_reverse_step(const float* x_dev, const float* w_out_dev,
+                                   const float* x_t_dev, const float* noise_dev,
+                                   float* eps_dev, float* x_prev_dev,
+                                   int32_t frames, int32_t h, int32_t w, int32_t c,
+                                   int32_t patch, int32_t dim, double coef_eps,
+                                   double inv_sqrt_alpha, double sqrt_beta,
+                                   void* stream);
+
 /* The tcgen05 GEMM on its own: out[m][n] = sum_k A[m][k] B[n][k]
  * (+ bias[n]) (+ resid[m][n]), A/B bf16 K-major (row pitch lda/ldb elements,
  * 16-byte aligned), fp32 accumulation and output. The projection GEMMs of the

@@ -296,6 +296,29 @@ class ToyDenoiser:
 
 
 # ---------------------------------------------------------------------------
+# diffusion.py -- schedule and the ancestral reverse step
+# ---------------------------------------------------------------------------
+
+def make_linear_schedule(steps, beta_start=1e-4, beta_end=0.02):
+    """diffusion.py:56-66 + NoiseSchedule diffusion.py:17-53 -> dict of arrays."""
+    betas = (np.array([beta_start]) if steps == 1
+             else np.linspace(beta_start, beta_end, steps, dtype=np.float64))
+    alphas = 1.0 - betas
+    abar = np.cumprod(alphas)
+    return {"betas": betas, "alphas": alphas, "alpha_bars": abar, "omab": 1.0 - abar}
+
+
+def reverse_step(schedule, x_t, t, predicted_noise, injected_noise=None):
+    """diffusion.py:95-116 -- x_t -> x_{t-1}; no noise at t == 1."""
+    i = t - 1
+    beta, alpha, omab = schedule["betas"][i], schedule["alphas"][i], schedule["omab"][i]
+    mean = (x_t - (beta / np.sqrt(omab)) * predicted_noise) / np.sqrt(alpha)
+    if t == 1 or injected_noise is None:
+        return mean
+    return mean + np.sqrt(beta) * injected_noise
+
+
+# ---------------------------------------------------------------------------
 # executor.py -- shard maps (integer, exact)
 # ---------------------------------------------------------------------------
 

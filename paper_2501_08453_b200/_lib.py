@@ -49,6 +49,8 @@ SIGNATURES = {
     "vc_layer_norm_f32": (C.c_int, [_p, _p, _i64, _i32, _p]),
     "vc_embed_frames": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _d, _p]),
     "vc_unembed_frames": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32, _p]),
+    "vc_unembed_reverse_step": (C.c_int, [_p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32,
+                                          _d, _d, _d, _p]),
     "vc_embed_frames_rows": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _d, _p]),
     "vc_gemm_bf16": (C.c_int, [_p, _i64, _p, _i64, _p, _p, _p, _i64, _i64, _i32, _i32, _p]),
     "vc_block_forward_launches": (C.c_int, [_S]),

@@ -149,10 +149,12 @@ static int block_forward_f32(const Dims& d, const char* packed, const float* x,
   }
   profile_mark(st, "attn_spatial");
   // temporal: sequence l = rows l, l+Lv, ..., l+(F-1)Lv
-  if (d.dh % 2 == 0) {
-    VC_TRY((launch_temporal_attn<float, float>(qkv + 3 * D, ld, D, acat + D, 3 * D, (int)d.F, (int)d.Lv,
-                                               (int)d.H, (int)d.dh, st)));
-  } else {  // odd head dims (tiny test shapes): generic strided kernel
+  int trc = VC_ENOTSUP;
+  if (d.dh % 2 == 0)
+    trc = launch_temporal_attn<float, float>(qkv + 3 * D, ld, D, acat + D, 3 * D, (int)d.F, (int)d.Lv,
+                                             (int)d.H, (int)d.dh, st);
+  if (trc != VC_OK && trc != VC_ENOTSUP) return trc;
+  if (trc == VC_ENOTSUP) {  // odd head dims / very long clips: generic strided kernel
     AttnArgs<float, float> a{};
     a.q = qkv + 3 * D; a.ldq = ld; a.q_seq_stride = 1; a.q_tok_stride = d.Lv;
     a.k = qkv + 4 * D; a.v = qkv + 5 * D; a.ldk = ld; a.k_seq_stride = 1; a.k_tok_stride = d.Lv;
@@ -391,6 +393,16 @@ int vc_unembed_frames(const float* x, const float* w_out, float* eps, int32_t F,
                       int32_t w, int32_t c, int32_t patch, int32_t dim, void* stream) {
   if (F < 1 || h < 1 || w < 1 || c < 1 || patch < 1) { set_error("bad latent shape"); return VC_EINVAL; }
   return launch_unembed(x, w_out, eps, F, h, w, c, patch, dim, (cudaStream_t)stream);
+}
+
+int vc_unembed_reverse_step(const float* x, const float* w_out, const float* x_t, const float* noise,
+                            float* eps, float* x_prev, int32_t F, int32_t h, int32_t w, int32_t c,
+                            int32_t patch, int32_t dim, double coef_eps, double inv_sqrt_alpha,
+                            double sqrt_beta, void* stream) {
+  if (F < 1 || h < 1 || w < 1 || c < 1 || patch < 1) { set_error("bad latent shape"); return VC_EINVAL; }
+  if (!x_t || !x_prev) { set_error("reverse step needs x_t and x_prev"); return VC_EINVAL; }
+  ReverseStep rs{x_t, noise, x_prev, (float)coef_eps, (float)inv_sqrt_alpha, (float)sqrt_beta};
+  return launch_unembed(x, w_out, eps, F, h, w, c, patch, dim, (cudaStream_t)stream, rs);
 }
 
 int vc_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, const float* bias,

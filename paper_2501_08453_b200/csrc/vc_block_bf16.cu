@@ -95,7 +95,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_attn_tc(a, sc.sp.q, sc.sp.k, sc.sp.vt, (int)F, Lv, Lv, wl.Lv_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_spatial");
-  VC_TRY((launch_temporal_attn<bf, bf>(tm, 3 * D, D, acat + D, 3 * D, (int)F, (int)Lv, (int)H, (int)dh, st)));
+  VC_TRY(launch_temporal_mma(tm, 3 * D, D, acat + D, 3 * D, (int)F, (int)Lv, (int)H, (int)dh, st));
   profile_mark(st, "attn_temporal");
   {
     AttnTcParams a{};

@@ -24,12 +24,17 @@
 namespace vc {
 
 namespace {
-constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
+// as many smem stages as fit next to the barriers / bias staging (4..6)
+template <int BN>
+constexpr int stages_for() {
+  return (216 * 1024) / (BM * BK * 2 + BN * BK * 2) > 8 ? 8 : (216 * 1024) / (BM * BK * 2 + BN * BK * 2);
+}
 constexpr int kThreads = 256;
 
 template <int BN>
 constexpr size_t smem_bytes() {
-  return (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 128 /*barriers*/ + 4 * 256 * 4 /*bias*/ +
+  return (size_t)stages_for<BN>() * (BM * BK * 2 + BN * BK * 2) + 256 /*barriers*/ + 4 * 256 * 4 /*bias*/ +
          1024 /*align*/;
 }
 
@@ -180,6 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const GemmTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int STAGES = stages_for<BN>();
   constexpr uint32_t kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
   constexpr int kBSlice = BN / CM;  // B rows each CTA loads and multicasts
   static_assert(kBSlice % 8 == 0, "B slice must keep 8-row swizzle atoms");
@@ -421,7 +427,8 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
               (long long)lda, (long long)ldb);
     return VC_EINVAL;
   }
-  if (bn == 0) bn = gemm_tc_pick_bn(p.N);
+  static const int bn_env = getenv("VC_GEMM_BN") ? atoi(getenv("VC_GEMM_BN")) : 0;  // tuning switch
+  if (bn == 0) bn = bn_env ? bn_env : gemm_tc_pick_bn(p.N);
   // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
   // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
   static const bool no_mc = getenv("VC_GEMM_NO_MC") != nullptr;

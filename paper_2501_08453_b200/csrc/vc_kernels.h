@@ -23,14 +23,26 @@ template <typename T, typename OutT>
 int launch_temporal_attn(const T* qkv, int64_t ld, int64_t D, OutT* o, int64_t ldo, int F, int Lv,
                          int H, int dh, cudaStream_t st);
 
+// bf16 temporal branch on warp-level tensor-core MMAs (vc_attn_temporal_mma.cu)
+int launch_temporal_mma(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo,
+                        int F, int Lv, int H, int dh, cudaStream_t st);
+
 template <typename OutT>
 int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
                    cudaStream_t st);
 
 int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int tok0,
                  int ntok, int h, int w, int c, int p, int D, double t, cudaStream_t st);
+// Optional DDPM reverse step fused into the unembed (diffusion.py:95-116):
+// x_prev = (x_t - coef_eps * eps) * inv_sqrt_alpha (+ sqrt_beta * noise)
+struct ReverseStep {
+  const float* x_t;
+  const float* noise;  // null: mean only (t == 1 or no injected noise)
+  float* x_prev;       // null: plain unembed
+  float coef_eps, inv_sqrt_alpha, sqrt_beta;
+};
 int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h, int w, int c,
-                   int p, int D, cudaStream_t st);
+                   int p, int D, cudaStream_t st, ReverseStep rs = ReverseStep{});
 // Column space of the bf16 QKV GEMM: the spatial / full-sequence Q, K, V
 // segments are head-padded (H heads x DP columns, dh real + DP-dh zero
 // weight columns) so every 16-column chunk of the GEMM tile lies inside one

@@ -114,7 +114,8 @@ __global__ void embed_kernel(const float* __restrict__ lat, const float* __restr
 // pixels (the crop).
 template <int PD>
 __global__ void unembed_kernel(const float* __restrict__ x, const float* __restrict__ w_out,
-                               float* __restrict__ eps, int F, int h, int w, int c, int p, int D) {
+                               float* __restrict__ eps, int F, int h, int w, int c, int p, int D,
+                               ReverseStep rs) {
   const int gh = (h + p - 1) / p, gw = (w + p - 1) / p;
   const int Lv = gh * gw, pd = p * p * c;
   const int lane = threadIdx.x & 31;
@@ -139,7 +140,15 @@ __global__ void unembed_kernel(const float* __restrict__ x, const float* __restr
     if (j >= pd || lane != (j & 31)) continue;
     const int py = j / (p * c), px = (j / c) % p, ch = j % c;
     const int yy = gy * p + py, xx = gx * p + px;
-    if (yy < h && xx < w) eps[(((int64_t)f * h + yy) * w + xx) * c + ch] = acc[j];
+    if (yy < h && xx < w) {
+      const int64_t px_i = (((int64_t)f * h + yy) * w + xx) * c + ch;
+      if (eps) eps[px_i] = acc[j];
+      if (rs.x_prev) {  // fused ancestral step, diffusion.py:95-116
+        float v = (rs.x_t[px_i] - rs.coef_eps * acc[j]) * rs.inv_sqrt_alpha;
+        if (rs.noise) v = fmaf(rs.sqrt_beta, rs.noise[px_i], v);
+        rs.x_prev[px_i] = v;
+      }
+    }
   }
 }
 
@@ -157,13 +166,13 @@ int launch_embed(const float* lat, const float* w_in, float* x, int F, int first
 }
 
 int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h, int w, int c,
-                   int p, int D, cudaStream_t st) {
+                   int p, int D, cudaStream_t st, ReverseStep rs) {
   const int64_t toks = (int64_t)F * ((h + p - 1) / p) * ((w + p - 1) / p);
   const int pd = p * p * c;
   if (toks <= 0) return VC_OK;
   dim3 grid((unsigned)cdiv(toks, 8));
-  if (pd <= 16) unembed_kernel<16><<<grid, 256, 0, st>>>(x, w_out, eps, F, h, w, c, p, D);
-  else if (pd <= 64) unembed_kernel<64><<<grid, 256, 0, st>>>(x, w_out, eps, F, h, w, c, p, D);
+  if (pd <= 16) unembed_kernel<16><<<grid, 256, 0, st>>>(x, w_out, eps, F, h, w, c, p, D, rs);
+  else if (pd <= 64) unembed_kernel<64><<<grid, 256, 0, st>>>(x, w_out, eps, F, h, w, c, p, D, rs);
   else {
     set_error("unembed supports patch*patch*channels <= 64, got %d", pd);
     return VC_ENOTSUP;

@@ -248,8 +248,7 @@ int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loca
     VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
     profile_mark(st, "sp_qkv_gemm");
     // temporal branch is rank-local: sequence = local position, tokens = frames (stride vc)
-    VC_TRY((launch_temporal_attn<bf, bf>(tm, 3 * x.D, x.D, acat + x.D, 3 * x.D, (int)x.F, vc, (int)x.H,
-                                         (int)x.dh, st)));
+    VC_TRY(launch_temporal_mma(tm, 3 * x.D, x.D, acat + x.D, 3 * x.D, (int)x.F, vc, (int)x.H, (int)x.dh, st));
     profile_mark(st, "sp_attn_temporal");
   }
   return VC_OK;

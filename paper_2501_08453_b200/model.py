@@ -142,6 +142,7 @@ class DeviceBlock:
                               for br in block.branches() for a in br.arrays()])
         lib = _lib.load()
         self.shape = _lib.shape(1, 1, 0, dim, heads, dtype)
+        _lib.check(lib.vc_block_shape_check(C.byref(self.shape)), "block shape")
         if raw.size != lib.vc_block_raw_weight_floats(C.byref(self.shape)):
             raise ValueError(f"block weights do not match dim {dim}")
         nbytes = lib.vc_block_packed_weight_bytes(C.byref(self.shape))
@@ -390,6 +391,33 @@ class ToyDenoiser:
         as_numpy = not _is_torch(latents)
         x = self.head_states_device(latents, t, prompt, dtype=dtype)
         return x.double().cpu().numpy() if as_numpy else x
+
+    def denoise_step(self, latents, t, prompt, schedule, injected_noise=None, *, dtype=None):
+        """One full sampling step x_t -> x_{t-1}: forward (model.py:327-333)
+        with the reference's reverse_step (diffusion.py:95-116) fused into the
+        unembed kernel (vc_unembed_reverse_step). At t == 1 or without
+        injected noise the step returns the mean, as the reference does.
+        Returns (x_prev, eps)."""
+        torch = _lib.require_cuda()
+        as_numpy = not _is_torch(latents)
+        F, h, w, c = latents.shape
+        coef_eps, inv_sqrt_alpha, sqrt_beta = schedule.reverse_coefficients(int(t))
+        xt = to_device_f32(torch, latents)
+        x = self.head_states_device(xt, t, prompt, dtype=dtype)
+        w_out = to_device_f32(torch, self.w_out)
+        eps = torch.empty((F, h, w, c), dtype=torch.float32, device="cuda")
+        x_prev = torch.empty_like(eps)
+        noise = None
+        if injected_noise is not None and int(t) != 1:
+            noise = to_device_f32(torch, injected_noise)
+        lib = _lib.load()
+        _lib.check(lib.vc_unembed_reverse_step(_lib.ptr(x), _lib.ptr(w_out), _lib.ptr(xt), _lib.ptr(noise),
+                                               _lib.ptr(eps), _lib.ptr(x_prev), F, h, w, c, self.spec.patch,
+                                               self.dim, float(coef_eps), float(inv_sqrt_alpha),
+                                               float(sqrt_beta), _lib.stream_ptr(torch)), "denoise step")
+        if as_numpy:
+            return x_prev.double().cpu().numpy(), eps.double().cpu().numpy()
+        return x_prev, eps
 
     def forward(self, latents, t, prompt, *, dtype=None):
         """model.py:327-333 -- predict the noise in a latent video [F, h, w, c]."""

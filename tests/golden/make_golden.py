@@ -99,6 +99,20 @@ def main():
         fixtures[f"{name}_out"] = model.forward(lat, t, prompt)
         print(name, "done", flush=True)
 
+    # --- one full sampling step on the config-1 model (diffusion.py:95-116) -
+    from spsim.diffusion import make_linear_schedule, reverse_step
+    sched = make_linear_schedule(100)
+    spec = rm.PatchSpec(8, 2, 4)
+    model = rm.ToyDenoiser.init(rn.SeededRng(2501), spec, 256, 4, 2)
+    data = rn.SeededRng(2501).split(DATA_TAG)
+    lat = data.split(1).normal((4, 16, 16, 4))
+    prompt = data.split(2).normal((32, 256))
+    z = data.split(3).normal((4, 16, 16, 4))
+    for t in (37, 1):
+        eps = model.forward(lat, t, prompt)
+        fixtures[f"rev_t{t}"] = reverse_step(sched, lat, t, eps, z)
+    fixtures["sched100_betas"] = sched.betas
+
     # --- integer shard maps (exact) --------------------------------------
     rows = []
     for n in (1, 2, 3, 5, 7, 32, 36, 64, 256, 1350, 1351):

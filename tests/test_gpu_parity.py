@@ -149,6 +149,21 @@ def test_model_forward_bf16_config1(vc):
     assert rel_l2(got, G["cfg1_out"]) <= BF16_TOL
 
 
+def test_denoise_step_fused_reverse_step(vc):
+    # forward + reverse_step (diffusion.py:95-116) fused into the unembed,
+    # against the reference's own step (golden), t = 37 with noise and t = 1
+    from paper_2501_08453_b200.diffusion import make_linear_schedule
+    model, lat, prompt = model_case(vc, "cfg1", 2501, 4, 16, 16, 32, 256, 4, 2)
+    z = vc.SeededRng(2501).split(DATA_TAG).split(3).normal((4, 16, 16, 4))
+    sched = make_linear_schedule(100)
+    for t in (37, 1):
+        x_prev, eps = model.denoise_step(lat, t, prompt, sched, z)
+        assert normwise(x_prev, G[f"rev_t{t}"]) <= FP32_TOL
+        assert normwise(eps, model.forward(lat, t, prompt)) <= 1e-6
+    x16, _ = model.denoise_step(lat, 37, prompt, sched, z, dtype="bf16")
+    assert rel_l2(x16, G["rev_t37"]) <= BF16_TOL
+
+
 def test_weight_mutation_is_seen(vc):
     # reference tests/test_model.py:256-262 mutates w_out in place
     model, lat, prompt = model_case(vc, "cfg1", 2501, 4, 16, 16, 32, 256, 4, 2)
@@ -216,3 +231,15 @@ def test_host_stream_matches_device_forward(vc):
         for i in range(5):
             ref = vc.parallel_block_forward(blk, x * (i + 1), vc.anchor_text(prompt, F), H, dtype=dt)
             assert np.array_equal(outs[i].double().numpy(), ref), (dt, i)
+
+
+@pytest.mark.parametrize("F,Lv,D,H", [(16, 40, 1584, 24), (37, 9, 256, 2), (64, 8, 3072, 24), (160, 3, 1584, 24)])
+def test_temporal_branch_long_clips(vc, F, Lv, D, H):
+    # frame-axis attention over 16..160 frames (configs 2, 4, 5): tensor-core
+    # (bf16) and smem / generic (fp32) kernels against the oracle
+    r = vc.SeededRng(F * 1000 + D)
+    p = vc.BranchParams.init(r.split(1), D)
+    x = r.normal((F, Lv, D))
+    ref = O.temporal_branch(O.BranchParams(*p.arrays()), x, H)
+    assert normwise(vc.temporal_branch(p, x, H, dtype="fp32"), ref) <= FP32_TOL
+    assert rel_l2(vc.temporal_branch(p, x, H, dtype="bf16"), ref) <= BF16_TOL

@@ -72,6 +72,31 @@ def test_model_forward_matches_reference(case):
     np.testing.assert_allclose(model.forward(lat, t, prompt), G[f"{name}_out"], atol=1e-11, rtol=0)
 
 
+def test_reverse_step_matches_reference():
+    # one ancestral sampling step on the config-1 model (diffusion.py:95-116)
+    sched = O.make_linear_schedule(100)
+    assert np.array_equal(sched["betas"], G["sched100_betas"])
+    model = O.ToyDenoiser.init(O.SeededRng(2501), O.PatchSpec(8, 2, 4), 256, 4, 2)
+    data = O.SeededRng(2501).split(DATA_TAG)
+    lat = data.split(1).normal((4, 16, 16, 4))
+    prompt = data.split(2).normal((32, 256))
+    z = data.split(3).normal((4, 16, 16, 4))
+    for t in (37, 1):
+        got = O.reverse_step(sched, lat, t, model.forward(lat, t, prompt), z)
+        np.testing.assert_allclose(got, G[f"rev_t{t}"], atol=1e-10, rtol=0)
+
+
+def test_product_schedule_constants_match_reference():
+    from paper_2501_08453_b200.diffusion import make_linear_schedule
+    s = make_linear_schedule(100)
+    assert np.array_equal(s.betas, G["sched100_betas"])
+    o = O.make_linear_schedule(100)
+    assert np.array_equal(s.alpha_bars, o["alpha_bars"]) and np.array_equal(s.one_minus_alpha_bars, o["omab"])
+    import pytest as _pt
+    with _pt.raises(ValueError):
+        s.reverse_coefficients(0)
+
+
 def test_contiguous_bounds_exact():
     flat = G["cb_flat"]
     pos = 0
