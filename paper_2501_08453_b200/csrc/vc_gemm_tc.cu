@@ -314,6 +314,157 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- CTA-pair GEMM (tcgen05 cta_group::2) ------------------------------------------
+// A cluster of 2 CTAs on one TPC computes a 256 x BN tile: each CTA TMAs its
+// 128 A rows and BN/2 B rows; the leader issues M=256 MMAs that read both
+// CTAs' shared memory and write each CTA's TMEM (its 128 rows x BN columns).
+// Per SM the operand bytes per MMA cycle drop by a third against the
+// single-CTA tile (B is split across the pair instead of replicated), which is
+// what limits the single-CTA kernel (L2 -> SMEM feed, ~96 B/clk needed).
+template <int BN>
+constexpr int stages2_for() {
+  return (216 * 1024) / (BM * BK * 2 + (BN / 2) * BK * 2) > 8 ? 8 : (216 * 1024) / (BM * BK * 2 + (BN / 2) * BK * 2);
+}
+template <int BN>
+constexpr size_t smem2_bytes() {
+  return (size_t)stages2_for<BN>() * (BM * BK * 2 + (BN / 2) * BK * 2) + 256 + 4 * 256 * 4 + 1024;
+}
+
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmTcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int STAGES = stages2_for<BN>();
+  constexpr int BNH = BN / 2;
+  static_assert(BNH % 8 == 0, "half tile must keep 8-row swizzle atoms");
+  constexpr uint32_t kABytes = BM * BK * 2, kBBytes = BNH * BK * 2;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * kBBytes);
+  uint64_t* full = bars;                // leader's: both CTAs' bytes
+  uint64_t* empty = bars + STAGES;      // each CTA's: leader MMA commit multicast
+  uint64_t* tfull = bars + 2 * STAGES;  // each CTA's
+  uint64_t* tempty = tfull + 2;         // leader's: both CTAs' epilogues
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias_all = reinterpret_cast<float*>(bars + 2 * STAGES + 8);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int num_m = (int)cdiv(p.M, 2 * BM), num_n = (int)cdiv(p.N, BN);
+  const int tiles = num_m * num_n;
+  const int kblocks = (int)cdiv(p.K, BK);
+
+  if (warp == 0 && ptx::elect_one()) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    // full[s] (leader): one arrival, the leader's expect_tx of BOTH CTAs' bytes
+    // (the peer's TMA may land first: the tx count just dips below zero)
+    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    // tempty (leader): one arrival per epilogue warp of both CTAs
+    for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * 4); }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, 512);
+  ptx::fence_before_sync();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      int s = 0; uint32_t ph = 0;
+      for (int t = cluster; t < tiles; t += nclusters) {
+        int mt, nt;
+        tile_coords(t, num_m, num_n, mt, nt);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * (kABytes + kBBytes));
+          ptx::tma_load_2d_2sm(sA + s * kABytes, &tmA, &full[s], kb * BK, mt * 2 * BM + rank * BM);
+          ptx::tma_load_2d_2sm(sB + s * kBBytes, &tmB, &full[s], kb * BK, nt * BN + rank * BNH);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BN);
+      int s = 0; uint32_t ph = 0; int local = 0;
+      for (int t = cluster; t < tiles; t += nclusters, ++local) {
+        const int acc = local & 1;
+        ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        ptx::fence_after_sync();
+        const uint32_t dtmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&full[s], ph);
+          ptx::fence_after_sync();
+          if (ptx::elect_one()) {
+            const uint32_t a0 = ptx::smem_u32(sA + s * kABytes);
+            const uint32_t b0 = ptx::smem_u32(sB + s * kBBytes);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad = ptx::smem_desc(a0 + kk * 32, 0, 1024, ptx::kLayoutSW128);
+              const uint64_t bd = ptx::smem_desc(b0 + kk * 32, 0, 1024, ptx::kLayoutSW128);
+              ptx::mma_bf16_ss_2sm(dtmem, ad, bd, idesc, (kb | kk) != 0);
+            }
+            ptx::mma_commit_2sm_mc(&empty[s], 0x3);
+            if (kb == kblocks - 1) ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
+          }
+          __syncwarp();
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int lane = threadIdx.x & 31;
+    float* sbias = sbias_all + q * 256;
+    const uint32_t tempty_leader = ptx::mapa_shared(ptx::smem_u32(tempty), 0);
+    int local = 0;
+    for (int t = cluster; t < tiles; t += nclusters, ++local) {
+      const int acc = local & 1;
+      int mt, nt;
+      tile_coords(t, num_m, num_n, mt, nt);
+      if (p.bias) {
+        __syncwarp();
+        for (int c = lane; c < BN; c += 32) {
+          const int n = nt * BN + c;
+          sbias[c] = n < p.N ? __ldg(p.bias + n) : 0.f;
+        }
+        __syncwarp();
+      }
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::fence_after_sync();
+      const int64_t mrow0 = (int64_t)mt * 2 * BM + rank * BM;
+      const int64_t m = mrow0 + q * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int c = 0; c < BN / 16; ++c) {
+        const int n0 = nt * BN + c * 16;
+        if (n0 >= p.N || mrow0 >= p.M) break;
+        uint32_t r[16];
+        ptx::tmem_ld16(tbase + c * 16, r);
+        ptx::tmem_ld_wait();
+        epilogue_chunk<EPI>(p, m, n0, r, p.bias ? sbias + c * 16 : nullptr);
+      }
+      ptx::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+    }
+  }
+  ptx::fence_before_sync();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::fence_after_sync();
+    ptx::tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
 // ---- host side -------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -363,6 +514,22 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   VC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, EPI, CM>, ta, tb, p));
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
+template <int BN, int EPI>
+int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t st) {
+  static bool attr_set = false;
+  constexpr size_t smem = smem2_bytes<BN>();
+  if (!attr_set) {
+    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    attr_set = true;
+  }
+  const int64_t tiles = cdiv(p.M, 2 * BM) * cdiv(p.N, BN);
+  const int pairs = (int)std::min<int64_t>(tiles, num_sms() / 2);
+  gemm_tc2_kernel<BN, EPI><<<2 * pairs, kThreads, smem, st>>>(ta, tb, p);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
@@ -432,12 +599,18 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
   // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
   static const bool no_mc = getenv("VC_GEMM_NO_MC") != nullptr;
+  // default: CTA-pair kernel (cta_group::2, 256-row tiles); VC_GEMM_1SM=1
+  // selects the single-CTA kernel with B multicast (A/B switch for profiling)
+  static const bool one_sm = getenv("VC_GEMM_1SM") != nullptr;
+  const bool pair = !one_sm && epi != EPI_BF16 && cdiv(p.M, BM) >= 2;
   const int cm = (!no_mc && epi != EPI_BF16 && cdiv(p.M, BM) >= 2) ? 2 : 1;
   CUtensorMap ta, tb;
   VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
-  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn / cm, CU_TENSOR_MAP_SWIZZLE_128B));
+  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn / (pair ? 2 : cm), CU_TENSOR_MAP_SWIZZLE_128B));
 #define VC_GEMM_CASE(BNV)                                                                    \
   if (bn == BNV) {                                                                           \
+    if (pair) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32>(ta, tb, p, st)              \
+                                    : launch_impl2<BNV, EPI_QKV>(ta, tb, p, st);             \
     if (epi == EPI_BF16) return launch_impl<BNV, EPI_BF16, 1>(ta, tb, p, st);                \
     if (epi == EPI_F32)                                                                      \
       return cm == 2 ? launch_impl<BNV, EPI_F32, 2>(ta, tb, p, st)                           \
