@@ -400,14 +400,27 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
   if (p.Lq <= 0 || nseq <= 0) return VC_OK;
   if (p.Lk <= 0) { set_error("attention needs at least one key"); return VC_EINVAL; }
   if (nseq > 65535 || p.H > 65535) { set_error("attention grid too large"); return VC_ENOTSUP; }
-  const bool one_tile = getenv("VC_ATTN_ONE_TILE") != nullptr;  // A/B switch for profiling
+  // A/B switches for profiling (VC_ATTN_IMPL): 1 one query tile per CTA, 2 one
+  // softmax thread per row, 3 (default) split rows with P in smem, 4 split rows with Q/P in
+  // TMEM, 5 64-key blocks with S double-buffered in TMEM, 6 one tile with S
+  // triple-buffered and four softmax warps per row.  3 is the default: the
+  // fastest measured (profiles/r01/README.md has the per-variant numbers).
+  static const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 3;
   switch (DP) {
     case 64:
-      if (!one_tile) return launch_attn_tc2<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 1) return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 2) return launch_attn_tc2<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 3) return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 4) return launch_attn_tc4<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 5) return launch_attn_tc5<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_attn_tc6<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 80:
-      if (!one_tile) return launch_attn_tc2<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 1) return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 2) return launch_attn_tc2<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 3) return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 4) return launch_attn_tc4<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 5) return launch_attn_tc5<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_attn_tc6<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 128: return launch_dp<128>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
   }
   set_error("tcgen05 attention: unsupported padded head dim %d", DP);

@@ -1,16 +1,21 @@
-// Flash attention, two query tiles per CTA ping-ponging on one tensor core
-// (the FA4 schedule) for padded head dims DP <= 80 (the 2B shape: dh 66 -> 80).
+// Flash attention, two query tiles per CTA ping-ponging on one tensor core,
+// each tile's softmax split across TWO warpgroups ("split rows").
 //
-// Same semantics and layouts as vc_attn_tc.cu (see there).  One CTA = 256
-// queries (tiles A, B) of one (sequence, head); every K/V tile TMA'd into
-// smem serves both query tiles.  384 threads:
-//   w0 TMA producer (Q_A, Q_B once; K and V rings of 3 stages each)
-//   w1 MMA issuer:  S_A(j+1) | PV_A(j) | S_B(j+1) | PV_B(j) per key tile
-//   w2 TMEM owner (512 cols: S_A 0, O_A 128, S_B 256, O_B 384)
-//   w4..w7  softmax of tile A, w8..w11 softmax of tile B (thread = row)
-// While one tile's softmax runs (MUFU / FMA bound) the tensor core works on
-// the other tile, and two softmax warps per SM sub-partition hide each
-// other's latencies.
+// Same semantics, layouts and MMA schedule as vc_attn_tc2.cu (DP <= 80: the
+// 2B shape dh 66 -> 80).  What changes is the softmax: in vc_attn_tc2 one
+// thread owns a query row's 128 logits of a key tile, and the measured
+// per-tile chain (TMEM load -> row max -> TMEM reload -> 128 exp2 -> P store,
+// tools/attn_trace.cu) ran at ~0.3 instructions/clock per warp, so two
+// softmax warps per SM sub-partition left MUFU idle 45% of the time.  Here
+// the two threads that own a row (warps w and w+4: same TMEM lane quarter,
+// same sub-partition) take 64 logits each:
+//   * logits stay in registers (one TMEM load, S released at once),
+//   * the two partial row maxima meet through two spare TMEM columns and a
+//     64-thread named barrier (both threads then agree bit-exactly on the
+//     lazily tracked max, so P, alpha and l match the one-thread kernel),
+//   * four softmax warps per sub-partition hide each other's latencies.
+// 18 warps: w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w17 softmax
+// (w = 2 + 8*tile + 4*half + i; w % 4 is the TMEM lane quarter).
 #include "vc_attn_tc_common.cuh"
 
 namespace vc {
@@ -19,67 +24,65 @@ namespace {
 
 using namespace attn;
 
-constexpr int kThreads2 = 384;
-// Fraction of exponentials computed by the FMA-pipe polynomial instead of
-// MUFU.EX2: one pair in kPolyEvery (MUFU is the softmax limiter on B200).
+constexpr int kWarps3 = 18;
+constexpr int kThreads3 = kWarps3 * 32;
 #ifndef VC_POLY_EVERY
 #define VC_POLY_EVERY 4
 #endif
-constexpr int kPolyEvery = VC_POLY_EVERY;
+constexpr int kPolyEvery3 = VC_POLY_EVERY;
 
-// Optional per-phase clock64 trace of one CTA (tools/attn_trace.cu builds the
-// kernel with -DVC_ATTN_TRACE; never part of the library build).
 #ifdef VC_ATTN_TRACE
-__device__ unsigned long long g_attn_trace[3][256][8];
-#define VC_TR(cond, role, j, k)                                              \
+__device__ unsigned long long g_attn_trace3[17][256][8];
+#define VC_TR3(cond, role, j, k)                                             \
   do {                                                                       \
-    if ((cond) && (j) < 256) g_attn_trace[role][j][k] = clock64();          \
+    if ((cond) && (j) < 256) g_attn_trace3[role][j][k] = clock64();         \
   } while (0)
 #else
-#define VC_TR(cond, role, j, k) \
-  do {                          \
+#define VC_TR3(cond, role, j, k) \
+  do {                           \
   } while (0)
 #endif
 
 template <int DP>
-struct Cfg2 {
+struct Cfg3 {
   static constexpr int N64 = DP / 64;
   static constexpr int TAIL = DP % 64;
   static_assert(TAIL == 0 || TAIL == 16, "DP must be 64*n or 64*n+16");
+  static_assert(DP <= 80, "O + exchange columns must fit 256 TMEM columns per tile");
   static constexpr int QK_BYTES = BQ * DP * 2;
   static constexpr int V_BYTES = DP * BKV * 2;
   static constexpr int P_BYTES = BQ * BKV * 2;
   static constexpr int KS = 3;
-  static constexpr int OFF_Q = 0;                          // 2 tiles
-  static constexpr int OFF_K = OFF_Q + 2 * QK_BYTES;       // KS stages
-  static constexpr int OFF_V = OFF_K + KS * QK_BYTES;      // KS stages
-  static constexpr int OFF_P = OFF_V + KS * V_BYTES;       // 1 buffer per tile
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + 2 * QK_BYTES;
+  static constexpr int OFF_V = OFF_K + KS * QK_BYTES;
+  static constexpr int OFF_P = OFF_V + KS * V_BYTES;
   static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int KSTEPS = DP / 16;
+  static constexpr int NC = DP / 16;       // 16-column chunks of O
+  static constexpr int NC0 = (NC + 1) / 2;  // chunks [0, NC0) -> half 0, rest -> half 1
+  static constexpr int XCOL = 208;          // exchange columns (after O's <= 80)
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-// ONES: V's first padding column (d == dh) holds 1.0 (vc_rowops.cu pack), so
-// O[:, dh] accumulates the softmax row sum on the tensor core and the softmax
-// warps skip the sum entirely.
 template <int DP, int POLY, bool ONES>
-__global__ void __launch_bounds__(kThreads2, 1)
-    attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
+__global__ void __launch_bounds__(kThreads3, 1)
+    attn_tc3_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                     const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
                     const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
-  using CF = Cfg2<DP>;
+  using CF = Cfg3<DP>;
   constexpr int KS = CF::KS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;      // [KS]
-  uint64_t* k_empty = k_full + KS;  // [KS]  both tiles' S MMAs done with it
+  uint64_t* k_empty = k_full + KS;  // [KS]
   uint64_t* v_full = k_empty + KS;  // [KS]
-  uint64_t* v_empty = v_full + KS;  // [KS]  both tiles' PV MMAs done with it
+  uint64_t* v_empty = v_full + KS;  // [KS]
   uint64_t* s_full = v_empty + KS;  // [2 tiles]
-  uint64_t* s_empty = s_full + 2;   // [2 tiles] softmax has read S
+  uint64_t* s_empty = s_full + 2;   // [2 tiles] both halves hold S in registers
   uint64_t* p_full = s_empty + 2;   // [2 tiles]
   uint64_t* pv_done = p_full + 2;   // [2 tiles]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
@@ -103,13 +106,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&s_empty[t], 128);
-      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&s_empty[t], 256);
+      ptx::mbar_init(&p_full[t], 256);
       ptx::mbar_init(&pv_done[t], 1);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
   ptx::fence_before_sync();
   __syncthreads();
   ptx::fence_after_sync();
@@ -147,7 +150,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKV);
     constexpr uint32_t idO = ptx::idesc_bf16_f32(BQ, DP);
     ptx::mbar_wait(q_full, 0);
-    // S_t(j) = Q_t K(j)^T into the tile's S columns
     auto issue_s = [&](int t, int j) {
       const int ks = j % KS;
       if (j > 0) ptx::mbar_wait(&s_empty[t], (j - 1) & 1);
@@ -159,11 +161,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
         for (int c = 0; c < CF::KSTEPS; ++c)
           ptx::mma_bf16_ss(tmem + t * 256, qk_desc<DP>(aQ, c), qk_desc<DP>(aK, c), idS, c > 0);
         ptx::mma_commit(&s_full[t]);
-        if (t == 1) ptx::mma_commit(&k_empty[ks]);  // covers both tiles' S MMAs
+        if (t == 1) ptx::mma_commit(&k_empty[ks]);
       }
       __syncwarp();
     };
-    // O_t += P_t(j) V(j)
     auto issue_pv = [&](int t, int j) {
       const int ks = j % KS;
       ptx::mbar_wait(&p_full[t], j & 1);
@@ -178,134 +179,128 @@ __global__ void __launch_bounds__(kThreads2, 1)
           ptx::mma_bf16_ss(tmem + t * 256 + 128, ad, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
         }
         ptx::mma_commit(&pv_done[t]);
-        if (t == 1) ptx::mma_commit(&v_empty[ks]);  // covers both tiles' PV MMAs
+        if (t == 1) ptx::mma_commit(&v_empty[ks]);
       }
       __syncwarp();
     };
+    const bool trm = tr && (threadIdx.x & 31) == 0;
     ptx::mbar_wait(&k_full[0], 0);
     issue_s(0, 0);
     issue_s(1, 0);
     for (int j = 0; j < n_tiles; ++j) {
       const bool more = j + 1 < n_tiles;
       if (more) ptx::mbar_wait(&k_full[(j + 1) % KS], ((j + 1) / KS) & 1);
-      VC_TR(tr && (threadIdx.x & 31) == 0, 0, j, 0);
+      VC_TR3(trm, 0, j, 0);
       ptx::mbar_wait(&v_full[j % KS], (j / KS) & 1);
-      VC_TR(tr && (threadIdx.x & 31) == 0, 0, j, 1);
+      VC_TR3(trm, 0, j, 1);
       if (more) issue_s(0, j + 1);
-      VC_TR(tr && (threadIdx.x & 31) == 0, 0, j, 2);
+      VC_TR3(trm, 0, j, 2);
       issue_pv(0, j);
-      VC_TR(tr && (threadIdx.x & 31) == 0, 0, j, 3);
+      VC_TR3(trm, 0, j, 3);
       if (more) issue_s(1, j + 1);
-      VC_TR(tr && (threadIdx.x & 31) == 0, 0, j, 4);
+      VC_TR3(trm, 0, j, 4);
       issue_pv(1, j);
-      VC_TR(tr && (threadIdx.x & 31) == 0, 0, j, 5);
+      VC_TR3(trm, 0, j, 5);
     }
-  } else if (warp >= 4) {
-    // ===================== softmax (tile t), correction, epilogue =====================
-    const int t = (warp - 4) >> 2;
-    const int qw = warp & 3;
+  } else {
+    // ===================== softmax (tile t, key half), correction, epilogue =====================
+    const int sw = warp - 2;
+    const int t = sw >> 3;
+    const int half = (sw >> 2) & 1;
+    const int quarter = warp & 3;
     const int lane = threadIdx.x & 31;
-    const int row = qw * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(qw * 32) << 16;
-    const uint32_t tS = tmem + t * 256 + lane_off;
-    const uint32_t tO = tS + 128;
-    const uint32_t sP = ptx::smem_u32(smem + CF::OFF_P + t * CF::P_BYTES);
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + t * 256 + lane_off + half * 64;
+    const uint32_t tO = tmem + t * 256 + 128 + lane_off;
+    const uint32_t tX = tmem + t * 256 + CF::XCOL + lane_off;
+    const uint32_t bar_id = 1 + t * 4 + quarter;
+    const uint32_t rowp = ptx::smem_u32(smem + CF::OFF_P + t * CF::P_BYTES) + half * (BQ * 128) + row * 128;
+    const bool trs = tr && lane == 0;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
-      const int k0 = j * BKV;
-      const bool slow = k0 < p.n_bias || k0 + BKV > p.Lk;  // warp-uniform: text keys / tail mask
+      const int kt = j * BKV;
+      const int k0 = kt + half * 64;
+      const bool slow = kt < p.n_bias || kt + BKV > p.Lk;  // tile-uniform: text keys / tail mask
       ptx::mbar_wait(&s_full[t], j & 1);
       ptx::fence_after_sync();
-      VC_TR(tr && row == 0, 1 + t, j, 0);
-      // pass 1 (TMEM -> registers, 64 logits at a time): row max
-      float mx = -INFINITY;
-#pragma unroll
-      for (int h64 = 0; h64 < 2; ++h64) {
-        uint32_t r[64];
-        ptx::tmem_ld32(tS + h64 * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
-        ptx::tmem_ld32(tS + h64 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-        ptx::tmem_ld_wait();
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      VC_TR3(trs, 1 + sw, j, 0);
+      uint32_t r[64];
+      ptx::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(r));
+      ptx::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+      ptx::tmem_ld_wait();
+      ptx::fence_before_sync();
+      ptx::mbar_arrive(&s_empty[t]);  // S lives in registers now
+      if (slow) {
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
-          float x = __uint_as_float(r[i]);
-          if (slow) {
-            const int key = k0 + h64 * 64 + i;
-            x *= p.scale_log2;
-            if (key < p.n_bias) x += p.bias_log2;
-            if (key >= p.Lk) x = -INFINITY;
-          }
-          m4[i & 3] = fmaxf(m4[i & 3], x);
+          float x = __uint_as_float(r[i]) * p.scale_log2;
+          if (k0 + i < p.n_bias) x += p.bias_log2;
+          if (k0 + i >= p.Lk) x = -INFINITY;
+          r[i] = __float_as_uint(x);
         }
-        mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
       }
-      if (!slow) mx *= p.scale_log2;
-      VC_TR(tr && row == 0, 1 + t, j, 1);
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 64; ++i) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(r[i]));
+      float pm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      if (!slow) pm *= p.scale_log2;
+      // partial maxima of the row's two halves meet in TMEM (parity-buffered)
+      const uint32_t xc = tX + 2 * (j & 1);
+      ptx::tmem_st1(xc + half, __float_as_uint(pm));
+      ptx::tmem_st_wait();
+      ptx::fence_before_sync();
+      ptx::named_bar_sync(bar_id, 64);
+      ptx::fence_after_sync();
+      uint32_t other;
+      ptx::tmem_ld1(xc + (half ^ 1), other);
+      ptx::tmem_ld_wait();
+      const float mx = fmaxf(pm, __uint_as_float(other));
+      VC_TR3(trs, 1 + sw, j, 1);
       float alpha = 1.f;
       if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
         alpha = ptx::ex2(m_used - mx);         // 0 on the first tile
         m_used = mx;
       }
-      // single P buffer per tile: PV_t(j-1) must be done reading it (and O
-      // must hold P(j-1)V(j-1) before a rescale)
-      if (j > 0) {
+      if (j > 0) {  // single P buffer per tile: PV_t(j-1) must be done with it
         ptx::mbar_wait(&pv_done[t], (j - 1) & 1);
         ptx::fence_after_sync();
       }
-      VC_TR(tr && row == 0, 1 + t, j, 2);
-      // pass 2: p = 2^(s*scale - m) (FFMA2 + MUFU), row sum, bf16 P -> smem
+      VC_TR3(trs, 1 + sw, j, 2);
       const float sc = slow ? 1.f : p.scale_log2;
       const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m_used, -m_used);
       float2 s2 = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
+      uint32_t pk[32];
 #pragma unroll
-      for (int h64 = 0; h64 < 2; ++h64) {
-        uint32_t r[64];
-        ptx::tmem_ld32(tS + h64 * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
-        ptx::tmem_ld32(tS + h64 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-        ptx::tmem_ld_wait();
-        if (h64 == 1) {  // S fully consumed: the MMA warp may overwrite it
-          ptx::fence_before_sync();
-          ptx::mbar_arrive(&s_empty[t]);
+      for (int i = 0; i < 64; i += 2) {
+        float2 e = ptx::ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nm2);
+        if (POLY > 0 && ((i >> 1) % (POLY > 0 ? POLY : 1)) == POLY - 1) {
+          e = ptx::ex2_poly2(e);
+        } else {
+          e.x = ptx::ex2(e.x);
+          e.y = ptx::ex2(e.y);
         }
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          float x0 = __uint_as_float(r[i]), x1 = __uint_as_float(r[i + 1]);
-          if (slow) {
-            const int key = k0 + h64 * 64 + i;
-            x0 *= p.scale_log2; x1 *= p.scale_log2;
-            if (key < p.n_bias) x0 += p.bias_log2;
-            if (key + 1 < p.n_bias) x1 += p.bias_log2;
-            if (key >= p.Lk) x0 = -INFINITY;
-            if (key + 1 >= p.Lk) x1 = -INFINITY;
-          }
-          float2 e = ptx::ffma2(make_float2(x0, x1), sc2, nm2);
-          if (POLY > 0 && ((i >> 1) % POLY) == POLY - 1) {
-            e = ptx::ex2_poly2(e);  // every POLY-th pair on the FMA pipe
-          } else {
-            e.x = ptx::ex2(e.x);
-            e.y = ptx::ex2(e.y);
-          }
-          if (!ONES) {
-            if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
-          }
-          pk[i >> 1] = ptx::bf16x2(e.x, e.y);
+        if (!ONES) {
+          if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
         }
-        const uint32_t rowp = sP + h64 * (BQ * 128) + row * 128;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        pk[i >> 1] = ptx::bf16x2(e.x, e.y);
       }
-      VC_TR(tr && row == 0, 1 + t, j, 3);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      VC_TR3(trs, 1 + sw, j, 3);
       if (!ONES) {
         s2 = ptx::fadd2(s2, s2b);
-        l = l * alpha + (s2.x + s2.y);
+        l = l * alpha + (s2.x + s2.y);  // this half's partial row sum
       }
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) rescale_o<DP>(tO, alpha);
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        if (half == 0) rescale_o<DP, 0, CF::NC0>(tO, alpha);
+        else rescale_o<DP, CF::NC0, CF::NC>(tO, alpha);
+      }
       ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
       ptx::fence_before_sync();
       ptx::mbar_arrive(&p_full[t]);
-      VC_TR(tr && row == 0, 1 + t, j, 4);
+      VC_TR3(trs, 1 + sw, j, 4);
     }
     ptx::mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
     ptx::fence_after_sync();
@@ -314,12 +309,23 @@ __global__ void __launch_bounds__(kThreads2, 1)
       ptx::tmem_ld1(tO + p.dh, r1);
       ptx::tmem_ld_wait();
       l = __uint_as_float(r1);
+    } else {  // the two halves' partial sums (same alpha history) add up
+      ptx::tmem_st1(tX + 4 + half, __float_as_uint(l));
+      ptx::tmem_st_wait();
+      ptx::fence_before_sync();
+      ptx::named_bar_sync(bar_id, 64);
+      ptx::fence_after_sync();
+      uint32_t other;
+      ptx::tmem_ld1(tX + 4 + (half ^ 1), other);
+      ptx::tmem_ld_wait();
+      l += __uint_as_float(other);
     }
-    store_out<DP>(p, tO, l, q0 + t * BQ + row, seq, h);
+    if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
+    else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
   }
   ptx::fence_before_sync();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     ptx::fence_after_sync();
     ptx::tmem_dealloc(tmem, 512);
   }
@@ -328,48 +334,47 @@ __global__ void __launch_bounds__(kThreads2, 1)
 }  // namespace
 
 #ifdef VC_ATTN_TRACE
-int attn_trace_read(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(g_attn_trace)) == cudaSuccess ? 0 : -1;
+int attn_trace3_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_attn_trace3, sizeof(g_attn_trace3)) == cudaSuccess ? 0 : -1;
 }
 #endif
 
 template <int DP>
-int launch_attn_tc2(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
                     int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
-  using CF = Cfg2<DP>;
+  using CF = Cfg3<DP>;
   AttnMaps m;
   VC_TRY(make_attn_maps<DP>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key));
-  static const int poly = getenv("VC_POLY_EVERY") ? atoi(getenv("VC_POLY_EVERY")) : kPolyEvery;
-  // the ones column exists iff the head dim is padded (V pad column dh = 1.0)
+  static const int poly = getenv("VC_POLY_EVERY") ? atoi(getenv("VC_POLY_EVERY")) : kPolyEvery3;
   static const bool no_ones = getenv("VC_NO_ONES_COLUMN") != nullptr;
   const bool ones = !no_ones && p.dh < DP;
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-#define VC_ATTN2_CASE(PV, ON)                                                                              \
+#define VC_ATTN3_CASE(PV, ON)                                                                              \
   if (poly == PV && ones == ON) {                                                                          \
     static bool attr = false;                                                                              \
     if (!attr) {                                                                                           \
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc2_kernel<DP, PV, ON>,                                      \
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc3_kernel<DP, PV, ON>,                                      \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));          \
       attr = true;                                                                                         \
     }                                                                                                      \
-    attn_tc2_kernel<DP, PV, ON><<<grid, kThreads2, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);   \
+    attn_tc3_kernel<DP, PV, ON><<<grid, kThreads3, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);   \
     VC_CHECK_LAUNCH();                                                                                     \
     return VC_OK;                                                                                          \
   }
-  VC_ATTN2_CASE(0, false)
-  VC_ATTN2_CASE(0, true)
-  VC_ATTN2_CASE(4, false)
-  VC_ATTN2_CASE(4, true)
-  VC_ATTN2_CASE(2, true)
-  VC_ATTN2_CASE(3, true)
-#undef VC_ATTN2_CASE
+  VC_ATTN3_CASE(0, false)
+  VC_ATTN3_CASE(0, true)
+  VC_ATTN3_CASE(4, false)
+  VC_ATTN3_CASE(4, true)
+  VC_ATTN3_CASE(2, true)
+  VC_ATTN3_CASE(3, true)
+#undef VC_ATTN3_CASE
   set_error("VC_POLY_EVERY must be 0 or 4 (2, 3 with the ones column)");
   return VC_EINVAL;
 }
 
-template int launch_attn_tc2<64>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,
+template int launch_attn_tc3<64>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,
                                  int64_t, int64_t, cudaStream_t);
-template int launch_attn_tc2<80>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,
+template int launch_attn_tc3<80>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,
                                  int64_t, int64_t, cudaStream_t);
 
 }  // namespace vc

@@ -16,14 +16,14 @@ constexpr float kRescaleThreshold = 8.0f;
 
 // smem descriptor of head-dim 16-chunk c of a [128 rows][DP] Q/K tile laid out
 // as N64 SW128 sub-tiles [128][128 B] followed by the SW32 tail [128][32 B]
-template <int DP>
+template <int DP, int ROWS = BQ>
 __device__ __forceinline__ uint64_t qk_desc(uint32_t tile_addr, int c) {
   constexpr int N64 = DP / 64;
   if (c < 4 * N64) {
-    const uint32_t a = tile_addr + (c >> 2) * (BQ * 128) + (c & 3) * 32;
+    const uint32_t a = tile_addr + (c >> 2) * (ROWS * 128) + (c & 3) * 32;
     return ptx::smem_desc(a, 0, 1024, ptx::kLayoutSW128);
   }
-  return ptx::smem_desc(tile_addr + N64 * (BQ * 128), 0, 256, ptx::kLayoutSW32);
+  return ptx::smem_desc(tile_addr + N64 * (ROWS * 128), 0, 256, ptx::kLayoutSW32);
 }
 
 // Load the row's 128 logits of S from TMEM (s_addr includes the lane offset).
@@ -84,10 +84,10 @@ __device__ __forceinline__ float softmax_step(float (&v)[BKV], int k0, const Att
 }
 
 // O (TMEM, DP fp32 columns of this lane) *= alpha
-template <int DP>
+template <int DP, int C0 = 0, int C1 = DP / 16>
 __device__ __forceinline__ void rescale_o(uint32_t o_addr, float alpha) {
 #pragma unroll
-  for (int c = 0; c < DP / 16; ++c) {
+  for (int c = C0; c < C1; ++c) {
     uint32_t r[16];
     ptx::tmem_ld16(o_addr + c * 16, r);
     ptx::tmem_ld_wait();
@@ -116,7 +116,8 @@ __device__ __forceinline__ void store_p(uint32_t p_tile, int row, const float (&
 
 // O / l -> bf16 -> output row of query qi of sequence seq, head h (plain
 // [row][ld_out] at col_off, or the sequence-parallel a2a #2 send layout).
-template <int DP>
+// C0..C1: the 16-column chunks of O this thread writes (all by default).
+template <int DP, int C0 = 0, int C1 = DP / 16>
 __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr, float l, int qi, int seq,
                                           int h) {
   const float inv = 1.f / l;
@@ -136,7 +137,7 @@ __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr
     }
   }
 #pragma unroll
-  for (int c = 0; c < DP / 16; ++c) {
+  for (int c = C0; c < C1; ++c) {
     uint32_t r[16];
     ptx::tmem_ld16(o_addr + c * 16, r);
     ptx::tmem_ld_wait();
@@ -157,11 +158,12 @@ __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr
   }
 }
 
-// TMA descriptors shared by both kernels (Q box rows = BQ, K box rows = BKV).
+// TMA descriptors shared by the kernels (Q box rows = BQ, K box rows = KROWS,
+// V^T box = 64 keys x DP).
 struct AttnMaps {
   CUtensorMap q64, q16, k64, k16, v;
 };
-template <int DP>
+template <int DP, int KROWS = BKV>
 inline int make_attn_maps(AttnMaps& m, const AttnTcParams& p, const void* q, const void* k, const void* vt,
                           int nseq, int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key) {
   constexpr bool TAIL = (DP % 64) != 0;
@@ -177,7 +179,7 @@ inline int make_attn_maps(AttnMaps& m, const AttnTcParams& p, const void* q, con
   {
     const uint64_t dims[4] = {(uint64_t)DP, (uint64_t)p.H, (uint64_t)p.Lk, (uint64_t)nseq};
     const uint64_t str[3] = {DP * eb, (uint64_t)p.H * DP * eb, (uint64_t)k_rows_per_seq * p.H * DP * eb};
-    const uint32_t box64[4] = {64, 1, BKV, 1}, box16[4] = {16, 1, BKV, 1};
+    const uint32_t box64[4] = {64, 1, KROWS, 1}, box16[4] = {16, 1, KROWS, 1};
     VC_TRY(make_tmap_4d_bf16(&m.k64, k, dims, str, box64, CU_TENSOR_MAP_SWIZZLE_128B));
     if (TAIL) VC_TRY(make_tmap_4d_bf16(&m.k16, k, dims, str, box16, CU_TENSOR_MAP_SWIZZLE_32B));
     else m.k16 = m.k64;
