@@ -233,16 +233,26 @@ def parallel_block_forward(block: BlockParams, visual, text, heads: int, *, dtyp
     return out.double().cpu().numpy() if as_numpy else out
 
 
-def block_forward_host_stream(block: BlockParams, visuals, prompt, heads: int, outs=None, *, dtype=None):
+def block_forward_host_stream(block, visuals, prompt, heads: int, outs=None, *, dtype=None):
     """Serving path: parallel_block_forward over a list of HOST batches (pinned
     float32 torch tensors [F, Lv, D]) with one shared prompt [Lt, D], through
     vc_block_forward_host_batched: H2D of batch i+1 and D2H of batch i-1
-    overlap the compute of batch i. Returns the list of host outputs."""
+    overlap the compute of batch i. Returns the list of host outputs.
+
+    `block` is a BlockParams (packed to the device on first use and re-packed
+    when its arrays change) or a DeviceBlock — the device-resident weight
+    handle a server keeps, which skips the per-call host-side change check."""
     torch = _lib.require_cuda()
-    dtype = _resolve_dtype(dtype)
+    if isinstance(block, DeviceBlock):
+        db = block
+        if heads != db.heads or (dtype is not None and _resolve_dtype(dtype) != db.dtype):
+            raise ValueError("heads / dtype disagree with the DeviceBlock")
+        dtype = db.dtype
+    else:
+        dtype = _resolve_dtype(dtype)
+        db = device_block(torch, block, heads, dtype)
     F, Lv, D = visuals[0].shape
     Lt = prompt.shape[0]
-    db = device_block(torch, block, heads, dtype)
     lib = _lib.load()
     shp = _lib.shape(F, Lv, Lt, D, heads, dtype)
     nbytes = lib.vc_block_stream_workspace_bytes(C.byref(shp))

@@ -231,6 +231,14 @@ def test_host_stream_matches_device_forward(vc):
         for i in range(5):
             ref = vc.parallel_block_forward(blk, x * (i + 1), vc.anchor_text(prompt, F), H, dtype=dt)
             assert np.array_equal(outs[i].double().numpy(), ref), (dt, i)
+        # the serving handle (device-resident packed weights) gives the same bits
+        from paper_2501_08453_b200.model import device_block
+        outs2 = block_forward_host_stream(device_block(torch, blk, H, dt), xs, pt, H)
+        torch.cuda.synchronize()
+        for i in range(5):
+            assert torch.equal(outs2[i], outs[i]), (dt, i)
+        with pytest.raises(ValueError):
+            block_forward_host_stream(device_block(torch, blk, H, dt), xs, pt, H + 1)
 
 
 @pytest.mark.parametrize("F,Lv,D,H", [(16, 40, 1584, 24), (37, 9, 256, 2), (64, 8, 3072, 24), (160, 3, 1584, 24)])
