@@ -62,15 +62,21 @@ struct Cfg3 {
   static constexpr int KSTEPS = DP / 16;
   static constexpr int NC = DP / 16;       // 16-column chunks of O
   static constexpr int NC0 = (NC + 1) / 2;  // chunks [0, NC0) -> half 0, rest -> half 1
-  static constexpr int XCOL = 208;          // exchange columns (after O's <= 80)
+  static constexpr int QCOL = 128 + DP;     // Q in TMEM (QT): DP/2 packed bf16x2 columns
+  static constexpr int XCOL = QCOL + DP / 2;  // exchange columns
+  static constexpr int QW = DP / 4;           // Q u32 words per half row
+  static_assert(XCOL + 6 <= 256, "per-tile TMEM columns");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, int POLY, bool ONES>
+// QT: Q lives in TMEM (loaded by the softmax threads, S MMA in the "ts" form
+// reading only K from shared memory) instead of smem (TMA, "ss" form).
+template <int DP, int POLY, bool ONES, bool QT>
 __global__ void __launch_bounds__(kThreads3, 1)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                     const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
-                    const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
+                    const __grid_constant__ CUtensorMap tmV, const __nv_bfloat16* __restrict__ qg,
+                    const int64_t q_rows_per_seq, const AttnTcParams p) {
   using CF = Cfg3<DP>;
   constexpr int KS = CF::KS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -92,12 +98,15 @@ __global__ void __launch_bounds__(kThreads3, 1)
   const int h = blockIdx.y;
   const int seq = blockIdx.z;
   const int n_tiles = (p.Lk + BKV - 1) / BKV;
+  // the last CTA of a sequence may have no rows in its second query tile
+  // (e.g. 1350 = 5 x 256 + 70): then only tile A runs (CTA-uniform)
+  const int ntile = q0 + BQ < p.Lq ? 2 : 1;
   [[maybe_unused]] const bool tr = blockIdx.x == 20 && blockIdx.y == 3 && blockIdx.z == 0;
 
   if (warp == 0 && ptx::elect_one()) {
     ptx::prefetch_tmap(&tmQ64); ptx::prefetch_tmap(&tmK64); ptx::prefetch_tmap(&tmV);
     if (CF::TAIL) { ptx::prefetch_tmap(&tmQ16); ptx::prefetch_tmap(&tmK16); }
-    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_full, QT ? 512 : 1);
     for (int i = 0; i < KS; ++i) {
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
@@ -121,8 +130,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (ptx::elect_one()) {
-      ptx::mbar_arrive_expect_tx(q_full, 2 * CF::QK_BYTES);
-      for (int t = 0; t < 2; ++t) {
+      if (!QT) ptx::mbar_arrive_expect_tx(q_full, 2 * CF::QK_BYTES);
+      for (int t = 0; t < 2 && !QT; ++t) {
         uint8_t* sQ = smem + CF::OFF_Q + t * CF::QK_BYTES;
         for (int c = 0; c < CF::N64; ++c)
           ptx::tma_load_4d(sQ + c * BQ * 128, &tmQ64, q_full, c * 64, h, q0 + t * BQ, seq);
@@ -158,10 +167,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const uint32_t aQ = ptx::smem_u32(smem + CF::OFF_Q + t * CF::QK_BYTES);
         const uint32_t aK = ptx::smem_u32(smem + CF::OFF_K + ks * CF::QK_BYTES);
 #pragma unroll
-        for (int c = 0; c < CF::KSTEPS; ++c)
-          ptx::mma_bf16_ss(tmem + t * 256, qk_desc<DP>(aQ, c), qk_desc<DP>(aK, c), idS, c > 0);
+        for (int c = 0; c < CF::KSTEPS; ++c) {
+          if (QT)
+            ptx::mma_bf16_ts(tmem + t * 256, tmem + t * 256 + CF::QCOL + 8 * c, qk_desc<DP>(aK, c), idS, c > 0);
+          else
+            ptx::mma_bf16_ss(tmem + t * 256, qk_desc<DP>(aQ, c), qk_desc<DP>(aK, c), idS, c > 0);
+        }
         ptx::mma_commit(&s_full[t]);
-        if (t == 1) ptx::mma_commit(&k_empty[ks]);
+        if (t == ntile - 1) ptx::mma_commit(&k_empty[ks]);
       }
       __syncwarp();
     };
@@ -179,14 +192,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
           ptx::mma_bf16_ss(tmem + t * 256 + 128, ad, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
         }
         ptx::mma_commit(&pv_done[t]);
-        if (t == 1) ptx::mma_commit(&v_empty[ks]);
+        if (t == ntile - 1) ptx::mma_commit(&v_empty[ks]);
       }
       __syncwarp();
     };
     const bool trm = tr && (threadIdx.x & 31) == 0;
     ptx::mbar_wait(&k_full[0], 0);
     issue_s(0, 0);
-    issue_s(1, 0);
+    if (ntile == 2) issue_s(1, 0);
     for (int j = 0; j < n_tiles; ++j) {
       const bool more = j + 1 < n_tiles;
       if (more) ptx::mbar_wait(&k_full[(j + 1) % KS], ((j + 1) / KS) & 1);
@@ -197,9 +210,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
       VC_TR3(trm, 0, j, 2);
       issue_pv(0, j);
       VC_TR3(trm, 0, j, 3);
-      if (more) issue_s(1, j + 1);
+      if (more && ntile == 2) issue_s(1, j + 1);
       VC_TR3(trm, 0, j, 4);
-      issue_pv(1, j);
+      if (ntile == 2) issue_pv(1, j);
       VC_TR3(trm, 0, j, 5);
     }
   } else {
@@ -214,114 +227,138 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const uint32_t tS = tmem + t * 256 + lane_off + half * 64;
     const uint32_t tO = tmem + t * 256 + 128 + lane_off;
     const uint32_t tX = tmem + t * 256 + CF::XCOL + lane_off;
+    if (QT) {  // this thread's half of its Q row -> TMEM (A operand of the S MMA)
+      const int qi = q0 + t * BQ + row;
+      uint32_t qv[CF::QW];
+      if (qi < p.Lq) {
+        const uint4* src = reinterpret_cast<const uint4*>(
+            qg + ((int64_t)seq * q_rows_per_seq + qi) * ((int64_t)p.H * DP) + (int64_t)h * DP + half * (DP / 2));
+#pragma unroll
+        for (int u = 0; u < CF::QW / 4; ++u) {
+          const uint4 w = __ldg(src + u);
+          qv[4 * u] = w.x; qv[4 * u + 1] = w.y; qv[4 * u + 2] = w.z; qv[4 * u + 3] = w.w;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < CF::QW; ++u) qv[u] = 0u;
+      }
+      const uint32_t tQ = tmem + t * 256 + lane_off + CF::QCOL + half * CF::QW;
+      ptx::tmem_st16(tQ, *reinterpret_cast<uint32_t(*)[16]>(qv));
+      if (CF::QW == 20) ptx::tmem_st4(tQ + 16, *reinterpret_cast<uint32_t(*)[4]>(qv + 16));
+      ptx::tmem_st_wait();
+      ptx::fence_before_sync();
+      ptx::mbar_arrive(q_full);
+    }
     const uint32_t bar_id = 1 + t * 4 + quarter;
     const uint32_t rowp = ptx::smem_u32(smem + CF::OFF_P + t * CF::P_BYTES) + half * (BQ * 128) + row * 128;
     const bool trs = tr && lane == 0;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int kt = j * BKV;
-      const int k0 = kt + half * 64;
-      const bool slow = kt < p.n_bias || kt + BKV > p.Lk;  // tile-uniform: text keys / tail mask
-      ptx::mbar_wait(&s_full[t], j & 1);
-      ptx::fence_after_sync();
-      VC_TR3(trs, 1 + sw, j, 0);
-      uint32_t r[64];
-      ptx::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(r));
-      ptx::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-      ptx::tmem_ld_wait();
-      ptx::fence_before_sync();
-      ptx::mbar_arrive(&s_empty[t]);  // S lives in registers now
-      if (slow) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          float x = __uint_as_float(r[i]) * p.scale_log2;
-          if (k0 + i < p.n_bias) x += p.bias_log2;
-          if (k0 + i >= p.Lk) x = -INFINITY;
-          r[i] = __float_as_uint(x);
-        }
-      }
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int i = 0; i < 64; ++i) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(r[i]));
-      float pm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-      if (!slow) pm *= p.scale_log2;
-      // partial maxima of the row's two halves meet in TMEM (parity-buffered)
-      const uint32_t xc = tX + 2 * (j & 1);
-      ptx::tmem_st1(xc + half, __float_as_uint(pm));
-      ptx::tmem_st_wait();
-      ptx::fence_before_sync();
-      ptx::named_bar_sync(bar_id, 64);
-      ptx::fence_after_sync();
-      uint32_t other;
-      ptx::tmem_ld1(xc + (half ^ 1), other);
-      ptx::tmem_ld_wait();
-      const float mx = fmaxf(pm, __uint_as_float(other));
-      VC_TR3(trs, 1 + sw, j, 1);
-      float alpha = 1.f;
-      if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
-        alpha = ptx::ex2(m_used - mx);         // 0 on the first tile
-        m_used = mx;
-      }
-      if (j > 0) {  // single P buffer per tile: PV_t(j-1) must be done with it
-        ptx::mbar_wait(&pv_done[t], (j - 1) & 1);
+    if (t < ntile) {  // a tile with no query rows has nothing to compute
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int kt = j * BKV;
+        const int k0 = kt + half * 64;
+        const bool slow = kt < p.n_bias || kt + BKV > p.Lk;  // tile-uniform: text keys / tail mask
+        ptx::mbar_wait(&s_full[t], j & 1);
         ptx::fence_after_sync();
-      }
-      VC_TR3(trs, 1 + sw, j, 2);
-      const float sc = slow ? 1.f : p.scale_log2;
-      const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m_used, -m_used);
-      float2 s2 = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
-      uint32_t pk[32];
-#pragma unroll
-      for (int i = 0; i < 64; i += 2) {
-        float2 e = ptx::ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nm2);
-        if (POLY > 0 && ((i >> 1) % (POLY > 0 ? POLY : 1)) == POLY - 1) {
-          e = ptx::ex2_poly2(e);
-        } else {
-          e.x = ptx::ex2(e.x);
-          e.y = ptx::ex2(e.y);
+        VC_TR3(trs, 1 + sw, j, 0);
+        uint32_t r[64];
+        ptx::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(r));
+        ptx::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        ptx::tmem_ld_wait();
+        ptx::fence_before_sync();
+        ptx::mbar_arrive(&s_empty[t]);  // S lives in registers now
+        if (slow) {
+  #pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            float x = __uint_as_float(r[i]) * p.scale_log2;
+            if (k0 + i < p.n_bias) x += p.bias_log2;
+            if (k0 + i >= p.Lk) x = -INFINITY;
+            r[i] = __float_as_uint(x);
+          }
         }
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  #pragma unroll
+        for (int i = 0; i < 64; ++i) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(r[i]));
+        float pm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        if (!slow) pm *= p.scale_log2;
+        // partial maxima of the row's two halves meet in TMEM (parity-buffered)
+        const uint32_t xc = tX + 2 * (j & 1);
+        ptx::tmem_st1(xc + half, __float_as_uint(pm));
+        ptx::tmem_st_wait();
+        ptx::fence_before_sync();
+        ptx::named_bar_sync(bar_id, 64);
+        ptx::fence_after_sync();
+        uint32_t other;
+        ptx::tmem_ld1(xc + (half ^ 1), other);
+        ptx::tmem_ld_wait();
+        const float mx = fmaxf(pm, __uint_as_float(other));
+        VC_TR3(trs, 1 + sw, j, 1);
+        float alpha = 1.f;
+        if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
+          alpha = ptx::ex2(m_used - mx);         // 0 on the first tile
+          m_used = mx;
+        }
+        if (j > 0) {  // single P buffer per tile: PV_t(j-1) must be done with it
+          ptx::mbar_wait(&pv_done[t], (j - 1) & 1);
+          ptx::fence_after_sync();
+        }
+        VC_TR3(trs, 1 + sw, j, 2);
+        const float sc = slow ? 1.f : p.scale_log2;
+        const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m_used, -m_used);
+        float2 s2 = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
+        uint32_t pk[32];
+  #pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          float2 e = ptx::ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nm2);
+          if (POLY > 0 && ((i >> 1) % (POLY > 0 ? POLY : 1)) == POLY - 1) {
+            e = ptx::ex2_poly2(e);
+          } else {
+            e.x = ptx::ex2(e.x);
+            e.y = ptx::ex2(e.y);
+          }
+          if (!ONES) {
+            if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
+          }
+          pk[i >> 1] = ptx::bf16x2(e.x, e.y);
+        }
+  #pragma unroll
+        for (int u = 0; u < 8; ++u)
+          ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        VC_TR3(trs, 1 + sw, j, 3);
         if (!ONES) {
-          if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
+          s2 = ptx::fadd2(s2, s2b);
+          l = l * alpha + (s2.x + s2.y);  // this half's partial row sum
         }
-        pk[i >> 1] = ptx::bf16x2(e.x, e.y);
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          if (half == 0) rescale_o<DP, 0, CF::NC0>(tO, alpha);
+          else rescale_o<DP, CF::NC0, CF::NC>(tO, alpha);
+        }
+        ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+        ptx::fence_before_sync();
+        ptx::mbar_arrive(&p_full[t]);
+        VC_TR3(trs, 1 + sw, j, 4);
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-      VC_TR3(trs, 1 + sw, j, 3);
-      if (!ONES) {
-        s2 = ptx::fadd2(s2, s2b);
-        l = l * alpha + (s2.x + s2.y);  // this half's partial row sum
-      }
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        if (half == 0) rescale_o<DP, 0, CF::NC0>(tO, alpha);
-        else rescale_o<DP, CF::NC0, CF::NC>(tO, alpha);
-      }
-      ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-      ptx::fence_before_sync();
-      ptx::mbar_arrive(&p_full[t]);
-      VC_TR3(trs, 1 + sw, j, 4);
-    }
-    ptx::mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
-    ptx::fence_after_sync();
-    if (ONES) {  // row sum accumulated by the tensor core in the ones column
-      uint32_t r1;
-      ptx::tmem_ld1(tO + p.dh, r1);
-      ptx::tmem_ld_wait();
-      l = __uint_as_float(r1);
-    } else {  // the two halves' partial sums (same alpha history) add up
-      ptx::tmem_st1(tX + 4 + half, __float_as_uint(l));
-      ptx::tmem_st_wait();
-      ptx::fence_before_sync();
-      ptx::named_bar_sync(bar_id, 64);
+      ptx::mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
       ptx::fence_after_sync();
-      uint32_t other;
-      ptx::tmem_ld1(tX + 4 + (half ^ 1), other);
-      ptx::tmem_ld_wait();
-      l += __uint_as_float(other);
+      if (ONES) {  // row sum accumulated by the tensor core in the ones column
+        uint32_t r1;
+        ptx::tmem_ld1(tO + p.dh, r1);
+        ptx::tmem_ld_wait();
+        l = __uint_as_float(r1);
+      } else {  // the two halves' partial sums (same alpha history) add up
+        ptx::tmem_st1(tX + 4 + half, __float_as_uint(l));
+        ptx::tmem_st_wait();
+        ptx::fence_before_sync();
+        ptx::named_bar_sync(bar_id, 64);
+        ptx::fence_after_sync();
+        uint32_t other;
+        ptx::tmem_ld1(tX + 4 + (half ^ 1), other);
+        ptx::tmem_ld_wait();
+        l += __uint_as_float(other);
+      }
+      if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
+      else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
     }
-    if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
-    else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
   }
   ptx::fence_before_sync();
   __syncthreads();
@@ -348,25 +385,36 @@ int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const v
   static const int poly = getenv("VC_POLY_EVERY") ? atoi(getenv("VC_POLY_EVERY")) : kPolyEvery3;
   static const bool no_ones = getenv("VC_NO_ONES_COLUMN") != nullptr;
   const bool ones = !no_ones && p.dh < DP;
+  // Q in TMEM (default) needs 16-byte aligned Q rows; VC_ATTN_QSMEM=1 keeps Q in smem
+  static const bool q_smem = getenv("VC_ATTN_QSMEM") && atoi(getenv("VC_ATTN_QSMEM")) != 0;
+  const bool qt = !q_smem && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+  const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-#define VC_ATTN3_CASE(PV, ON)                                                                              \
-  if (poly == PV && ones == ON) {                                                                          \
+#define VC_ATTN3_CASE(PV, ON, Q)                                                                           \
+  if (poly == PV && ones == ON && qt == Q) {                                                               \
     static bool attr = false;                                                                              \
     if (!attr) {                                                                                           \
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc3_kernel<DP, PV, ON>,                                      \
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc3_kernel<DP, PV, ON, Q>,                                   \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));          \
       attr = true;                                                                                         \
     }                                                                                                      \
-    attn_tc3_kernel<DP, PV, ON><<<grid, kThreads3, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);   \
+    attn_tc3_kernel<DP, PV, ON, Q><<<grid, kThreads3, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, qb,  \
+                                                                      q_rows_per_seq, p);                  \
     VC_CHECK_LAUNCH();                                                                                     \
     return VC_OK;                                                                                          \
   }
-  VC_ATTN3_CASE(0, false)
-  VC_ATTN3_CASE(0, true)
-  VC_ATTN3_CASE(4, false)
-  VC_ATTN3_CASE(4, true)
-  VC_ATTN3_CASE(2, true)
-  VC_ATTN3_CASE(3, true)
+  VC_ATTN3_CASE(0, false, false)
+  VC_ATTN3_CASE(0, true, false)
+  VC_ATTN3_CASE(4, false, false)
+  VC_ATTN3_CASE(4, true, false)
+  VC_ATTN3_CASE(2, true, false)
+  VC_ATTN3_CASE(3, true, false)
+  VC_ATTN3_CASE(0, false, true)
+  VC_ATTN3_CASE(0, true, true)
+  VC_ATTN3_CASE(4, false, true)
+  VC_ATTN3_CASE(4, true, true)
+  VC_ATTN3_CASE(2, true, true)
+  VC_ATTN3_CASE(3, true, true)
 #undef VC_ATTN3_CASE
   set_error("VC_POLY_EVERY must be 0 or 4 (2, 3 with the ones column)");
   return VC_EINVAL;
