@@ -281,17 +281,27 @@ __global__ void __launch_bounds__(kThreads3, 1)
         for (int i = 0; i < 64; ++i) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(r[i]));
         float pm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         if (!slow) pm *= p.scale_log2;
-        // partial maxima of the row's two halves meet in TMEM (parity-buffered)
-        const uint32_t xc = tX + 2 * (j & 1);
-        ptx::tmem_st1(xc + half, __float_as_uint(pm));
-        ptx::tmem_st_wait();
-        ptx::fence_before_sync();
-        ptx::named_bar_sync(bar_id, 64);
-        ptx::fence_after_sync();
-        uint32_t other;
-        ptx::tmem_ld1(xc + (half ^ 1), other);
-        ptx::tmem_ld_wait();
-        const float mx = fmaxf(pm, __uint_as_float(other));
+        // partial maxima of the row's two halves meet (parity-buffered) in the
+        // idle Q smem region when Q lives in TMEM, else in spare TMEM columns
+        float other;
+        if (QT) {
+          float* xs = reinterpret_cast<float*>(smem + CF::OFF_Q) + ((j & 1) * 2 * 2 + t * 2) * BQ;
+          xs[half * BQ + row] = pm;
+          ptx::named_bar_sync(bar_id, 64);
+          other = xs[(half ^ 1) * BQ + row];
+        } else {
+          const uint32_t xc = tX + 2 * (j & 1);
+          ptx::tmem_st1(xc + half, __float_as_uint(pm));
+          ptx::tmem_st_wait();
+          ptx::fence_before_sync();
+          ptx::named_bar_sync(bar_id, 64);
+          ptx::fence_after_sync();
+          uint32_t o;
+          ptx::tmem_ld1(xc + (half ^ 1), o);
+          ptx::tmem_ld_wait();
+          other = __uint_as_float(o);
+        }
+        const float mx = fmaxf(pm, other);
         VC_TR3(trs, 1 + sw, j, 1);
         float alpha = 1.f;
         if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
