@@ -118,6 +118,13 @@ class TorchExchange:
 class SPBlock:
     """One rank's share of a sequence-parallel block forward (bf16)."""
 
+    def launches_per_forward(self) -> int:
+        """Kernels this rank launches per forward (vc_sp.cu; NCCL's own not counted):
+        stage 1 LN + QKV GEMM + temporal, stage 2 unpack + text K/V GEMMs (2) +
+        spatial + full-sequence attention, stage 3 unpack + O GEMM."""
+        mr = self.F * (self.vb[self.rank + 1] - self.vb[self.rank])
+        return (3 if mr > 0 else 1) + 1 + (2 if self.Lt > 0 else 0) + 2 + (2 if mr > 0 else 0)
+
     def __init__(self, torch, device_block, frames, visual_len, text_len, nranks, rank):
         if device_block.dtype != "bf16":
             raise ValueError("sequence parallelism runs the bf16 path")
@@ -410,7 +417,7 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
             "e2e": {"value": Nv / (float(e2e.item()) / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(xh.numel() * 4) * world, "d2h_bytes_per_step": int(oh.numel() * 4) * world},
             "clocks": clk.summary(),
-            "gpu_launches": None,
+            "gpu_launches": spb.launches_per_forward() * args.steps,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
