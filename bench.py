@@ -495,6 +495,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sp", action="store_true",
                     help="run the sequence-parallel (NCCL) path even at world size 1")
+    ap.add_argument("--sp-mode", default="head_parallel", choices=["head_parallel", "gather"],
+                    help="SP attention: head-parallel all-to-alls (default) or K/V all-gather "
+                         "(chosen automatically when the GPU count does not divide the heads)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -224,6 +224,36 @@ VC_API int vc_sp_stage3(const vc_sp_plan* plan, const void* packed_dev,
                         void* workspace_dev, size_t workspace_bytes,
                         void* stream);
 
+/* ---- Gather-mode sequence parallelism -----------------------------------
+ * _branch_gather (executor.py:416-459), the plan.attention != "head_parallel"
+ * branch of _run_branch (:462-466): every rank all-gathers the spatial and
+ * full-sequence K,V of ALL heads and attends for its own rows, so P need not
+ * divide H (e.g. 4 heads on 8 ranks). Same shard map as above. The host runs
+ *   vc_spg_stage1 (writes this rank's slot of the gather buffer)
+ *   -> all_gather (vc_spg_slot_elems bf16 per rank, slot r at r*slot_elems)
+ *   -> vc_spg_stage2
+ * Exchange per rank: (P-1)/P of 4*Nv*D-ish bf16 (K,V of two branches), about
+ * 4x the head-parallel volume — head-parallel stays the default when H % P == 0. */
+/* validity: P <= Lv (executor.py:521-524), 1..16 ranks. */
+VC_API int vc_spg_check(const vc_sp_plan* plan);
+VC_API size_t vc_spg_workspace_bytes(const vc_sp_plan* plan);
+/* bf16 elements of one rank's slot (identical for every rank); -1 on error. */
+VC_API int64_t vc_spg_slot_elems(const vc_sp_plan* plan);
+/* x_local [F][vc_r][D] fp32, prompt [Lt][D] fp32 -> this rank's K,V slot
+ * (gather + rank * slot_elems); the local Q, the temporal branch and the
+ * text K,V of all heads (from the local prompt copy) stay in the workspace. */
+VC_API int vc_spg_stage1(const vc_sp_plan* plan, const void* packed_dev,
+                         const float* x_local_dev, const float* prompt_dev,
+                         void* gather_dev, void* workspace_dev,
+                         size_t workspace_bytes, void* stream);
+/* gathered K,V of all ranks -> attention of the local rows (all heads) ->
+ * O projection (+ x_local if add_residual) -> out_local fp32. */
+VC_API int vc_spg_stage2(const vc_sp_plan* plan, const void* packed_dev,
+                         const void* gather_dev, const float* x_local_dev,
+                         float* out_local_dev, int add_residual,
+                         void* workspace_dev, size_t workspace_bytes,
+                         void* stream);
+
 /* Stage profiler (bench accounting, not used on the timed path): when
  * enabled, vc_block_forward records a CUDA event after each of its kernels,
  * synchronises at the end of the call and accumulates per-stage device time

@@ -61,6 +61,11 @@ SIGNATURES = {
     "vc_sp_stage1": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _p, _sz, _p]),
     "vc_sp_stage2": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _sz, _p]),
     "vc_sp_stage3": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, C.c_int, _p, _sz, _p]),
+    "vc_spg_check": (C.c_int, [C.POINTER(SpPlan)]),
+    "vc_spg_workspace_bytes": (_sz, [C.POINTER(SpPlan)]),
+    "vc_spg_slot_elems": (_i64, [C.POINTER(SpPlan)]),
+    "vc_spg_stage1": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _p, _sz, _p]),
+    "vc_spg_stage2": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, C.c_int, _p, _sz, _p]),
     "vc_profile_enable": (C.c_int, [C.c_int]),
     "vc_profile_reset": (None, []),
     "vc_profile_read": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int32, C.c_char_p, C.c_size_t]),

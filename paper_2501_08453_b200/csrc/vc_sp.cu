@@ -42,7 +42,7 @@ struct Sp {
   QkvPad pad;
 };
 
-int sp_make(const vc_sp_plan* pl, Sp* o) {
+int sp_make(const vc_sp_plan* pl, Sp* o, bool gather = false) {
   if (!pl) { set_error("null plan"); return VC_EINVAL; }
   const vc_block_shape& s = pl->shape;
   VC_TRY(vc_block_shape_check(&s));
@@ -56,14 +56,15 @@ int sp_make(const vc_sp_plan* pl, Sp* o) {
     set_error("cannot spread %d visual tokens per frame over %d devices", s.visual_len, P);
     return VC_EINVAL;
   }
-  if (P > 1 && s.heads % P != 0) {  // executor.py:525-529
+  if (!gather && P > 1 && s.heads % P != 0) {  // executor.py:525-529
     set_error("head-parallel attention needs sp_size to divide %d heads, got %d", s.heads, P);
     return VC_EINVAL;
   }
   Sp& x = *o;
   x.F = s.frames; x.Lv = s.visual_len; x.Lt = s.text_len; x.D = s.dim; x.H = s.heads;
   x.dh = x.D / x.H; x.Nv = x.F * x.Lv; x.P = P; x.rank = pl->rank;
-  x.Hg = x.H / P; x.Dg = x.Hg * x.dh;
+  x.Hg = gather ? x.H : x.H / P;
+  x.Dg = x.Hg * x.dh;
   x.pad = qkv_pad_layout(x.D, x.H);
   x.DP = x.pad.DP;
   x.Lv_ld = round_up(x.Lv, 8);
@@ -180,6 +181,113 @@ __global__ void sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv, __nv_b
     const int g = (int)(gb / 2), bp = (int)(gb % 2);
     const uint32_t v = reinterpret_cast<const uint32_t*>(recv + row * Dg)[wi];
     reinterpret_cast<uint32_t*>(acat + m * 3 * D + bp * 2 * D + (int64_t)g * Dg)[wi] = v;
+  }
+}
+
+// ---- gather mode (executor.py:416-459) ----
+// One rank's slot of the gather buffer (identical size on every rank, local
+// row counts padded to vcmax = max_r vc_r):
+//   A  spatial K   [F][vcmax][H][DP]   (local row m = f*vc_r + l)
+//   B  spatial V^T [F][H][DP][vcl_ld]  (local key l)
+//   C  full-seq K  [F*vcmax][H][DP]    (local row m)
+//   Dv full-seq V^T [H][DP][fsl_ld]    (local key m)
+struct SpgSlot {
+  int64_t vcmax, vcl_ld, fsl_ld, A, B, C, Dv, total;  // offsets in bf16 elements
+};
+SpgSlot spg_slot(const Sp& x) {
+  SpgSlot g;
+  int vmax = 0;
+  for (int r = 0; r < x.P; ++r) vmax = std::max(vmax, x.vb[r + 1] - x.vb[r]);
+  g.vcmax = vmax;
+  g.vcl_ld = round_up(g.vcmax, 8);
+  g.fsl_ld = round_up(x.F * g.vcmax, 8);
+  const int64_t row = x.H * x.DP;
+  g.A = 0;
+  g.B = g.A + x.F * g.vcmax * row;
+  g.C = g.B + x.F * row * g.vcl_ld;
+  g.Dv = g.C + x.F * g.vcmax * row;
+  g.total = round_up(g.Dv + row * g.fsl_ld, 512);  // keep every slot 1 KB aligned
+  return g;
+}
+
+struct SpgWs {
+  size_t xhat, tm, qsp, qfs, ksp, vtsp, kfs, vtfs, acat, total;
+};
+SpgWs spg_ws(const Sp& x) {
+  SpgWs w;
+  const int64_t Mr = x.M[x.rank];
+  const size_t qk = (size_t)x.H * x.DP * 2;
+  size_t o = 0;
+  w.xhat = o; o = aup(o + (size_t)(Mr + x.Lt) * x.D * 2);
+  w.tm = o; o = aup(o + (size_t)Mr * 3 * x.D * 2);
+  w.qsp = o; o = aup(o + (size_t)Mr * qk);                       // local queries
+  w.qfs = o; o = aup(o + (size_t)Mr * qk);
+  w.ksp = o; o = aup(o + (size_t)x.Nv * qk);                     // global keys / values
+  w.vtsp = o; o = aup(o + (size_t)x.F * x.H * x.DP * x.Lv_ld * 2);
+  w.kfs = o; o = aup(o + (size_t)(x.Lt + x.Nv) * qk);
+  w.vtfs = o; o = aup(o + (size_t)x.H * x.DP * x.Lk_ld * 2);
+  w.acat = o; o = aup(o + (size_t)Mr * 3 * x.D * 2);
+  w.total = o;
+  return w;
+}
+
+struct SpgUnpack {
+  const __nv_bfloat16* gather;
+  int32_t P, F, Lv, Lt, H, DP;
+  int32_t vb[17];
+  int64_t slot, vcl_ld, fsl_ld, offA, offB, offC, offD, Lv_ld, Lk_ld;
+  __nv_bfloat16 *ksp, *vtsp, *kfs, *vtfs;
+};
+
+// K rows of every rank's slot -> global spatial K [F][Lv][H][DP] and full-seq
+// K [Lt + Nv][H][DP] (text rows untouched).  One warp per (rank, branch, row):
+// a row is H*DP bf16, copied as 16-byte vectors.
+__global__ void __launch_bounds__(256) spg_unpack_k_kernel(SpgUnpack a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t vec = (int64_t)a.H * a.DP / 8;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < 2LL * a.F * a.Lv; w += nw) {
+    const int b = (int)(w / ((int64_t)a.F * a.Lv));   // 0 spatial, 1 full sequence
+    const int64_t tok = w - (int64_t)b * a.F * a.Lv;   // global visual token f*Lv + l
+    const int f = (int)(tok / a.Lv), l = (int)(tok - (int64_t)f * a.Lv);
+    int r = 0;
+    while (l >= a.vb[r + 1]) ++r;
+    const int vc = a.vb[r + 1] - a.vb[r];
+    const int64_t m = (int64_t)f * vc + (l - a.vb[r]);
+    const uint4* src = reinterpret_cast<const uint4*>(a.gather + r * a.slot + (b == 0 ? a.offA : a.offC) +
+                                                      m * a.H * a.DP);
+    uint4* dst = reinterpret_cast<uint4*>(b == 0 ? a.ksp + tok * a.H * a.DP : a.kfs + (a.Lt + tok) * a.H * a.DP);
+    for (int64_t i = lane; i < vec; i += 32) dst[i] = src[i];
+  }
+}
+
+// V^T rows of every rank's slot -> global V^T.  Spatial: row (f, h, d) of rank
+// r holds keys [0, vc_r) -> keys [vb[r], vb[r+1]) of row (f, h, d) of
+// [F][H][DP][Lv_ld].  Full-seq: row (h, d) holds keys m = f*vc_r + l -> key
+// Lt + f*Lv + vb[r] + l of [H][DP][Lk_ld].  One block per (rank, branch, row),
+// threads over keys.
+__global__ void __launch_bounds__(256) spg_unpack_vt_kernel(SpgUnpack a) {
+  const int64_t hd = (int64_t)a.H * a.DP;
+  const int64_t per_rank = (int64_t)a.F * hd + hd;  // spatial rows + full-seq rows
+  for (int64_t job = blockIdx.x; job < a.P * per_rank; job += gridDim.x) {
+    const int r = (int)(job / per_rank);
+    const int64_t j = job - r * per_rank;
+    const int vc = a.vb[r + 1] - a.vb[r];
+    const __nv_bfloat16* base = a.gather + r * a.slot;
+    if (j < (int64_t)a.F * hd) {  // spatial row j = (f*H + h)*DP + d
+      const __nv_bfloat16* src = base + a.offB + j * a.vcl_ld;
+      __nv_bfloat16* dst = a.vtsp + j * a.Lv_ld + a.vb[r];
+      for (int l = threadIdx.x; l < vc; l += blockDim.x) dst[l] = src[l];
+    } else {  // full-sequence row (h, d)
+      const int64_t row = j - (int64_t)a.F * hd;
+      const __nv_bfloat16* src = base + a.offD + row * a.fsl_ld;
+      __nv_bfloat16* dst = a.vtfs + row * a.Lk_ld + a.Lt + a.vb[r];
+      const int64_t n = (int64_t)a.F * vc;
+      for (int64_t m = threadIdx.x; m < n; m += blockDim.x) {
+        const int f = (int)(m / vc);
+        dst[(int64_t)f * a.Lv + (m - (int64_t)f * vc)] = src[m];
+      }
+    }
   }
 }
 
@@ -340,6 +448,129 @@ int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, 
   g.out_f32 = out_local; g.ldo = x.D; g.R = add_residual ? x_local : nullptr; g.ldr = x.D;
   VC_TRY(launch_gemm_tc(acat, 3 * x.D, pp.wo, 3 * x.D, g, EPI_F32, st));
   profile_mark(st, "sp_oproj_gemm");
+  return VC_OK;
+}
+
+// ---- gather mode ----
+
+int vc_spg_check(const vc_sp_plan* plan) {
+  Sp x;
+  return sp_make(plan, &x, true);
+}
+
+size_t vc_spg_workspace_bytes(const vc_sp_plan* plan) {
+  Sp x;
+  if (sp_make(plan, &x, true) != VC_OK) return 0;
+  return spg_ws(x).total;
+}
+
+int64_t vc_spg_slot_elems(const vc_sp_plan* plan) {
+  Sp x;
+  if (sp_make(plan, &x, true) != VC_OK) return -1;
+  return spg_slot(x).total;
+}
+
+int vc_spg_stage1(const vc_sp_plan* plan, const void* packed, const float* x_local, const float* prompt,
+                  void* gather, void* ws, size_t ws_bytes, void* stream) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x, true));
+  const SpgWs w = spg_ws(x);
+  const SpgSlot gs = spg_slot(x);
+  if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* W = (char*)ws;
+  typedef __nv_bfloat16 bf;
+  const PackedPtrs pp = packed_ptrs(x, packed);
+  const int64_t Mr = x.M[x.rank];
+  const int vc = x.vb[x.rank + 1] - x.vb[x.rank];
+  bf* xhat = (bf*)(W + w.xhat);
+  bf* tm = (bf*)(W + w.tm);
+  bf* acat = (bf*)(W + w.acat);
+  bf* slot = (bf*)gather + x.rank * gs.total;
+  VC_TRY(launch_ln_rows<bf>(x_local, Mr, prompt, x.Lt, (int)x.D, xhat, st));
+  profile_mark(st, "spg_ln");
+  if (Mr > 0) {
+    // the block's QKV GEMM over the local rows with the local geometry (Lv :=
+    // vc_r, no text): Q stays here, K and V^T land in this rank's slot
+    GemmTcParams g{};
+    g.M = Mr; g.N = (int)x.pad.Npad; g.K = (int)x.D; g.bias = pp.bias;
+    QkvScatter& s = g.qkv;
+    s.pad = x.pad; s.D = x.D; s.Lv = vc; s.Lt = 0; s.H = (int)x.H; s.tm = tm;
+    s.sp = BranchOut{(bf*)(W + w.qsp), slot + gs.A, slot + gs.B, gs.vcl_ld};
+    s.fs = BranchOut{(bf*)(W + w.qfs), slot + gs.C, slot + gs.Dv, gs.fsl_ld};
+    VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
+    profile_mark(st, "spg_qkv_gemm");
+    VC_TRY(launch_temporal_mma(tm, 3 * x.D, x.D, acat + x.D, 3 * x.D, (int)x.F, vc, (int)x.H, (int)x.dh, st));
+    profile_mark(st, "spg_attn_temporal");
+  }
+  if (x.Lt > 0) {  // text K, V of all heads from the local prompt copy -> global full-seq keys [0, Lt)
+    const int64_t n0 = x.pad.fs_base() + x.pad.SEG;
+    GemmTcParams g{};
+    g.M = x.Lt; g.N = (int)(2 * x.pad.SEG); g.K = (int)x.D; g.bias = pp.bias + n0;
+    QkvScatter& s = g.qkv;
+    s.pad = x.pad; s.D = x.D; s.Lv = x.Lv; s.Lt = x.Lt; s.H = (int)x.H;
+    s.n_base = n0; s.text_rows = 1;
+    s.sp = BranchOut{nullptr, (bf*)(W + w.ksp), (bf*)(W + w.vtsp), x.Lv_ld};
+    s.fs = BranchOut{(bf*)(W + w.qfs), (bf*)(W + w.kfs), (bf*)(W + w.vtfs), x.Lk_ld};
+    VC_TRY(launch_gemm_tc(xhat + Mr * x.D, x.D, pp.wqkv + n0 * x.D, x.D, g, EPI_QKV, st));
+    profile_mark(st, "spg_text_kv_gemm");
+  }
+  return VC_OK;
+}
+
+int vc_spg_stage2(const vc_sp_plan* plan, const void* packed, const void* gather, const float* x_local,
+                  float* out_local, int add_residual, void* ws, size_t ws_bytes, void* stream) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x, true));
+  const SpgWs w = spg_ws(x);
+  const SpgSlot gs = spg_slot(x);
+  if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* W = (char*)ws;
+  typedef __nv_bfloat16 bf;
+  const PackedPtrs pp = packed_ptrs(x, packed);
+  const int64_t Mr = x.M[x.rank];
+  const int vc = x.vb[x.rank + 1] - x.vb[x.rank];
+  {
+    SpgUnpack a{};
+    a.gather = (const bf*)gather; a.P = (int)x.P; a.F = (int)x.F; a.Lv = (int)x.Lv; a.Lt = (int)x.Lt;
+    a.H = (int)x.H; a.DP = (int)x.DP;
+    for (int r = 0; r <= x.P; ++r) a.vb[r] = x.vb[r];
+    a.slot = gs.total; a.vcl_ld = gs.vcl_ld; a.fsl_ld = gs.fsl_ld;
+    a.offA = gs.A; a.offB = gs.B; a.offC = gs.C; a.offD = gs.Dv; a.Lv_ld = x.Lv_ld; a.Lk_ld = x.Lk_ld;
+    a.ksp = (bf*)(W + w.ksp); a.vtsp = (bf*)(W + w.vtsp); a.kfs = (bf*)(W + w.kfs); a.vtfs = (bf*)(W + w.vtfs);
+    const int64_t kwarps = 2 * x.F * x.Lv;
+    spg_unpack_k_kernel<<<(int)std::min<int64_t>(cdiv(kwarps, 8), 148 * 16), 256, 0, st>>>(a);
+    VC_CHECK_LAUNCH();
+    const int64_t vjobs = x.P * (x.F + 1) * x.H * x.DP;
+    spg_unpack_vt_kernel<<<(int)std::min<int64_t>(vjobs, 148 * 32), 256, 0, st>>>(a);
+    VC_CHECK_LAUNCH();
+    profile_mark(st, "spg_unpack");
+  }
+  if (Mr == 0) return VC_OK;
+  bf* acat = (bf*)(W + w.acat);
+  const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)x.dh));
+  {  // spatial: the local rows of every frame against all Lv keys of that frame
+    AttnTcParams a{};
+    a.Lq = vc; a.Lk = (int)x.Lv; a.H = (int)x.H; a.dh = (int)x.dh;
+    a.n_bias = 0; a.bias_log2 = 0.f; a.scale_log2 = scale_log2;
+    a.out = acat; a.ld_out = 3 * x.D; a.col_off = 0; a.out_seq_rows = vc;
+    VC_TRY(launch_attn_tc(a, W + w.qsp, W + w.ksp, W + w.vtsp, (int)x.F, vc, x.Lv, x.Lv_ld, (int)x.DP, st));
+    profile_mark(st, "spg_attn_spatial");
+  }
+  {  // full sequence: the local rows against the deduplicated text + all visual keys
+    AttnTcParams a{};
+    a.Lq = (int)Mr; a.Lk = (int)(x.Lt + x.Nv); a.H = (int)x.H; a.dh = (int)x.dh;
+    a.n_bias = (int)x.Lt; a.bias_log2 = (float)log2((double)x.F); a.scale_log2 = scale_log2;
+    a.out = acat; a.ld_out = 3 * x.D; a.col_off = 2 * x.D; a.out_seq_rows = 0;
+    VC_TRY(launch_attn_tc(a, W + w.qfs, W + w.kfs, W + w.vtfs, 1, Mr, x.Lt + x.Nv, x.Lk_ld, (int)x.DP, st));
+    profile_mark(st, "spg_attn_fullseq");
+  }
+  GemmTcParams g{};
+  g.M = Mr; g.N = (int)x.D; g.K = (int)(3 * x.D);
+  g.out_f32 = out_local; g.ldo = x.D; g.R = add_residual ? x_local : nullptr; g.ldr = x.D;
+  VC_TRY(launch_gemm_tc(acat, 3 * x.D, pp.wo, 3 * x.D, g, EPI_F32, st));
+  profile_mark(st, "spg_oproj_gemm");
   return VC_OK;
 }
 

@@ -110,6 +110,11 @@ class TorchExchange:
     def all_to_all(self, recv, send, recv_counts, send_counts):
         self.dist.all_to_all_single(recv, send, recv_counts, send_counts, group=self.group)
 
+    def all_gather(self, gather, rank):
+        """In place: gather is [P * slot]; this rank's slot is already filled."""
+        n = gather.numel() // self.dist.get_world_size(self.group)
+        self.dist.all_gather_into_tensor(gather, gather[rank * n:(rank + 1) * n], group=self.group)
+
 
 # ---------------------------------------------------------------------------
 # The rank-local CUDA stages
@@ -188,6 +193,88 @@ def run_stages(stages, x_local, prompt, out_local, exchange, add_residual=False)
     exchange.all_to_all(stages.recv2, stages.send2, stages.counts["recv2"], stages.counts["send2"])
     stages.stage3(x_local, out_local, add_residual)
     return out_local
+
+
+class SPGatherBlock:
+    """One rank's share of a GATHER-mode sequence-parallel block forward
+    (_branch_gather, executor.py:416-459): all-gather the spatial and
+    full-sequence K,V of all heads, attend for the own rows. No head
+    divisibility requirement (P need not divide H); about 4x the exchange
+    volume of the head-parallel mode, which stays the default."""
+
+    def __init__(self, torch, device_block, frames, visual_len, text_len, nranks, rank):
+        if device_block.dtype != "bf16":
+            raise ValueError("sequence parallelism runs the bf16 path")
+        self.torch = torch
+        self.db = device_block
+        D, H = device_block.dim, device_block.heads
+        if nranks > visual_len:
+            raise ValueError(f"cannot spread {visual_len} visual tokens per frame over {nranks} devices")
+        self.plan = _lib.SpPlan(_lib.shape(frames, visual_len, text_len, D, H, "bf16"), nranks, rank)
+        lib = _lib.load()
+        _lib.check(lib.vc_spg_check(C.byref(self.plan)), "sp plan")
+        self.F, self.Lv, self.Lt, self.D, self.H, self.P, self.rank = frames, visual_len, text_len, D, H, nranks, rank
+        self.vb = contiguous_bounds(visual_len, nranks)
+        self.slot = int(lib.vc_spg_slot_elems(C.byref(self.plan)))
+        self.gather = torch.empty(nranks * self.slot, dtype=torch.bfloat16, device="cuda")
+        self.ws_bytes = int(lib.vc_spg_workspace_bytes(C.byref(self.plan)))
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device="cuda")
+
+    @property
+    def local_rows(self):
+        return self.vb[self.rank], self.vb[self.rank + 1]
+
+    def launches_per_forward(self) -> int:
+        """stage 1 LN + QKV GEMM + temporal + text K/V GEMM, stage 2 two unpack
+        kernels + spatial + full-sequence attention + O GEMM (NCCL not counted)."""
+        mr = self.F * (self.vb[self.rank + 1] - self.vb[self.rank])
+        return 1 + (2 if mr > 0 else 0) + (1 if self.Lt > 0 else 0) + 2 + (3 if mr > 0 else 0)
+
+    def stage1(self, x_local, prompt):
+        lib = _lib.load()
+        _lib.check(lib.vc_spg_stage1(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(x_local),
+                                     _lib.ptr(prompt) if self.Lt else C.c_void_p(0), _lib.ptr(self.gather),
+                                     _lib.ptr(self.ws), self.ws_bytes, _lib.stream_ptr(self.torch)), "spg stage1")
+
+    def stage2(self, x_local, out_local, add_residual=False):
+        lib = _lib.load()
+        _lib.check(lib.vc_spg_stage2(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(self.gather),
+                                     _lib.ptr(x_local), _lib.ptr(out_local), 1 if add_residual else 0,
+                                     _lib.ptr(self.ws), self.ws_bytes, _lib.stream_ptr(self.torch)), "spg stage2")
+
+    def forward(self, x_local, prompt, out_local, exchange, add_residual=False):
+        return run_gather_stages(self, x_local, prompt, out_local, exchange, add_residual)
+
+
+def run_gather_stages(stages, x_local, prompt, out_local, exchange, add_residual=False):
+    """Gather-mode rank-local schedule: stage1 (this rank's K,V slot) ->
+    in-place all-gather of the slots -> stage2 (SPGatherBlock on the GPU; a
+    numpy stand-in in the CPU gloo test)."""
+    stages.stage1(x_local, prompt)
+    exchange.all_gather(stages.gather, stages.rank)
+    stages.stage2(x_local, out_local, add_residual)
+    return out_local
+
+
+def emulate_sp_gather_forward(torch, device_block, x, prompt, nranks, add_residual=False):
+    """Gather-mode SP block forward over P virtual ranks on one GPU (the
+    all-gather becomes slot copies; ranks never wait on one another)."""
+    F, Lv, D = x.shape
+    Lt = prompt.shape[0] if prompt is not None else 0
+    blocks = [SPGatherBlock(torch, device_block, F, Lv, Lt, nranks, r) for r in range(nranks)]
+    vb = blocks[0].vb
+    xs = [x[:, vb[r]:vb[r + 1]].contiguous() for r in range(nranks)]
+    outs = [torch.empty_like(t) for t in xs]
+    for r, b in enumerate(blocks):
+        b.stage1(xs[r], prompt)
+    n = blocks[0].slot
+    for g in range(nranks):  # every rank receives every slot
+        for r in range(nranks):
+            if r != g:
+                blocks[g].gather[r * n:(r + 1) * n].copy_(blocks[r].gather[r * n:(r + 1) * n])
+    for r, b in enumerate(blocks):
+        b.stage2(xs[r], outs[r], add_residual)
+    return torch.cat(outs, dim=1)
 
 
 class EmulatedRanks:
@@ -348,7 +435,14 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
     F, Lv, Lt, D, H, name = CONFIGS[args.config]
     blk = BlockParams.init(SeededRng(2025).split(1000), D)
     db = DeviceBlock(torch, blk, H, "bf16")
-    spb = SPBlock(torch, db, F, Lv, Lt, world, rank)
+    # head-parallel (the reference's default) unless P does not divide H or
+    # gather mode is asked for (executor.py:462-466)
+    mode = getattr(args, "sp_mode", "head_parallel")
+    if mode == "gather" or H % world != 0:
+        mode = "gather"
+        spb = SPGatherBlock(torch, db, F, Lv, Lt, world, rank)
+    else:
+        spb = SPBlock(torch, db, F, Lv, Lt, world, rank)
     lo, hi = spb.local_rows
     g = torch.Generator(device="cuda").manual_seed(2025)
     x_full = torch.randn((F, Lv, D), device="cuda", generator=g)  # same on every rank (same seed)
@@ -397,7 +491,10 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     flops = sum(algorithmic_flops(F, Lv, Lt, D, H).values())
     peaks = load_peaks()
-    a2a_bytes = 2 * (sum(spb.counts["send1"]) + sum(spb.counts["send2"]))  # bf16 bytes sent per rank
+    if mode == "gather":  # bf16 bytes sent per rank: own slot to every peer
+        a2a_bytes = 2 * spb.slot * (world - 1)
+    else:
+        a2a_bytes = 2 * (sum(spb.counts["send1"]) + sum(spb.counts["send2"]))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -406,13 +503,15 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
             "data": "synthetic (torch.randn inputs, SeededRng random-init 2B-shape weights)",
             "config": {"workload": name, "frames": F, "visual_len": Lv, "text_len": Lt, "dim": D, "heads": H,
                        "tokens_per_step": Nv,
-                       "parallelism": f"sequence parallel sp{world} (spatial shard axis, head-parallel a2a, NCCL)",
+                       "parallelism": (f"sequence parallel sp{world} (spatial shard axis, "
+                                       + ("head-parallel a2a" if mode == "head_parallel" else "K/V all-gather")
+                                       + ", NCCL)"),
                        "l2": "inputs larger than L2 on every rank"},
             "roofline": {"bound": "tensor", "kernel": "whole block (per GPU)",
                          "achieved": flops / world / (ms_per_step / 1e3) / 1e12, "peak": peaks["tc_sus"],
                          "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peaks["tc_sus"],
                          "traffic": None},
-            "a2a": {"bytes_sent_per_rank_per_step": a2a_bytes},
+            "a2a": {"mode": mode, "bytes_sent_per_rank_per_step": a2a_bytes},
             "cpu_baseline": None,
             "e2e": {"value": Nv / (float(e2e.item()) / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(xh.numel() * 4) * world, "d2h_bytes_per_step": int(oh.numel() * 4) * world},

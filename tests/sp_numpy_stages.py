@@ -92,3 +92,52 @@ class NumpyStages:
         if add_residual:
             y = y + x_local.numpy()
         out_local.copy_(torch.from_numpy(y))
+
+
+class NumpyGatherStages:
+    """Gather-mode stand-in (executor.py:416-459): slot of rank r =
+    [branch][k|v][F][vcmax][D] (all heads), all-gathered; stage 2 rebuilds every
+    sequence's keys in global order and attends for the own rows."""
+
+    def __init__(self, block, F, Lv, Lt, D, H, P, rank):
+        self.block, self.F, self.Lv, self.Lt, self.D, self.H, self.P, self.rank = block, F, Lv, Lt, D, H, P, rank
+        self.vb = sp.contiguous_bounds(Lv, P)
+        self.vcmax = max(self.vb[r + 1] - self.vb[r] for r in range(P))
+        self.slot = 2 * 2 * F * self.vcmax * D
+        self.gather = torch.zeros(P * self.slot, dtype=torch.float64)
+
+    def _slot(self, r):
+        return self.gather.numpy()[r * self.slot:(r + 1) * self.slot].reshape(2, 2, self.F, self.vcmax, self.D)
+
+    def stage1(self, x_local, prompt):
+        F, D = self.F, self.D
+        xl = x_local.numpy()
+        vc = xl.shape[1]
+        rows = xl.reshape(-1, D)
+        s = self._slot(self.rank)
+        self.q = []
+        for bp, params in enumerate((self.block.spatial, self.block.fullseq)):
+            q, k, v = O.branch_qkv(params, rows)
+            self.q.append(q)
+            s[bp, 0, :, :vc] = k.reshape(F, vc, D)
+            s[bp, 1, :, :vc] = v.reshape(F, vc, D)
+        self.a_tm = O.temporal_branch(self.block.temporal, xl, self.H)  # local: every frame of the own positions
+        self.prompt = prompt.numpy()
+
+    def stage2(self, x_local, out_local, add_residual=False):
+        F, Lv, Lt, D, H = self.F, self.Lv, self.Lt, self.D, self.H
+        vc = self.vb[self.rank + 1] - self.vb[self.rank]
+        full = np.zeros((2, 2, F, Lv, D))
+        for r in range(self.P):
+            n = self.vb[r + 1] - self.vb[r]
+            full[:, :, :, self.vb[r]:self.vb[r + 1]] = self._slot(r)[:, :, :, :n]
+        qs = self.q[0].reshape(F, vc, D)
+        out_sp = O.attention(qs, full[0, 0], full[0, 1], H) @ self.block.spatial.wo   # per frame
+        _, kt, vt = O.branch_qkv(self.block.fullseq, self.prompt)
+        K = np.concatenate([np.tile(kt, (F, 1)), full[1, 0].reshape(F * Lv, D)])     # F anchored text copies
+        V = np.concatenate([np.tile(vt, (F, 1)), full[1, 1].reshape(F * Lv, D)])
+        out_fs = (O.attention(self.q[1], K, V, H) @ self.block.fullseq.wo).reshape(F, vc, D)
+        y = out_sp + self.a_tm + out_fs
+        if add_residual:
+            y = y + x_local.numpy()
+        out_local.copy_(torch.from_numpy(y))

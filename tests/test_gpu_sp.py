@@ -54,6 +54,38 @@ def test_sp_matches_single_gpu_and_oracle(torch, shape, Ps):
     assert rel_l2(got, ref + x) <= 2e-2
 
 
+@pytest.mark.parametrize("shape,Ps", [((3, 64, 32, 256, 8), (1, 2, 3, 5, 8)),
+                                      ((4, 64, 32, 256, 4), (3, 8)),
+                                      ((2, 1350, 256, 1584, 24), (5, 8))],
+                         ids=["small_dh32", "4heads_P_ndiv_H", "2b_f2"])
+def test_sp_gather_mode_matches_single_gpu_and_oracle(torch, shape, Ps):
+    # gather-mode SP (_branch_gather, executor.py:416-459), P need
+    # not divide H (4 heads on 3 / 8 ranks, 24 heads on 5)
+    import paper_2501_08453_b200 as vc
+    from paper_2501_08453_b200 import sp
+    from paper_2501_08453_b200.model import DeviceBlock, block_forward_device
+    F, Lv, Lt, D, H = shape
+    blk = vc.BlockParams.init(vc.SeededRng(37).split(1000), D)
+    data = vc.SeededRng(37).split(1 << 20)
+    x = data.split(1).normal((F, Lv, D))
+    prompt = data.split(2).normal((Lt, D))
+    oblk = O.BlockParams(*[O.BranchParams(*b.arrays()) for b in blk.branches()])
+    ref = O.parallel_block_forward(oblk, x, O.anchor_text(prompt, F), H)
+    db = DeviceBlock(torch, blk, H, "bf16")
+    xt = torch.from_numpy(x.astype(np.float32)).cuda()
+    pt = torch.from_numpy(prompt.astype(np.float32)).cuda()
+    single = torch.empty_like(xt)
+    block_forward_device(torch, db, xt, pt, single, False)
+    single = single.double().cpu().numpy()
+    for P in Ps:
+        got = sp.emulate_sp_gather_forward(torch, db, xt, pt, P).double().cpu().numpy()
+        assert np.isfinite(got).all()
+        assert rel_l2(got, single) <= 1e-3, P
+        assert rel_l2(got, ref) <= 2e-2, P
+    got = sp.emulate_sp_gather_forward(torch, db, xt, pt, Ps[-1], add_residual=True).double().cpu().numpy()
+    assert rel_l2(got, ref + x) <= 2e-2
+
+
 def test_sp_rejects_bad_plans(torch):
     import paper_2501_08453_b200 as vc
     from paper_2501_08453_b200 import sp
