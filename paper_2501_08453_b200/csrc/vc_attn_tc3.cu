@@ -71,12 +71,16 @@ struct Cfg3 {
 
 // QT: Q lives in TMEM (loaded by the softmax threads, S MMA in the "ts" form
 // reading only K from shared memory) instead of smem (TMA, "ss" form).
-template <int DP, int POLY, bool ONES, bool QT>
+// PH (needs !QT): the P of keys [0, 64) (half 0) goes to TMEM over the idle
+// Q columns and the PV MMA reads it from there ("ts" k-steps 0..3); only keys
+// [64, 128) go through shared memory — half the P store + P operand traffic
+// on the SM's shared-memory port, the kernel's busiest shared resource.
+template <int DP, int POLY, bool ONES, bool QT, bool PH = false>
 __global__ void __launch_bounds__(kThreads3, 1)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                     const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
                     const __grid_constant__ CUtensorMap tmV, const __nv_bfloat16* __restrict__ qg,
-                    const int64_t q_rows_per_seq, const AttnTcParams p) {
+                    const int64_t q_rows_per_seq, const AttnTcParams p, const bool LOCK) {
   using CF = Cfg3<DP>;
   constexpr int KS = CF::KS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -189,7 +193,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
         for (int c = 0; c < BKV / 16; ++c) {
           const uint64_t ad = ptx::smem_desc(aP + (c >> 2) * (BQ * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
           const uint64_t bd = ptx::smem_desc(aV + (c >> 2) * (DP * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
-          ptx::mma_bf16_ss(tmem + t * 256 + 128, ad, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
+          if (PH && c < 4)
+            ptx::mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + CF::QCOL + 8 * c, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
+          else
+            ptx::mma_bf16_ss(tmem + t * 256 + 128, ad, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
         }
         ptx::mma_commit(&pv_done[t]);
         if (t == ntile - 1) ptx::mma_commit(&v_empty[ks]);
@@ -206,14 +213,28 @@ __global__ void __launch_bounds__(kThreads3, 1)
       VC_TR3(trm, 0, j, 0);
       ptx::mbar_wait(&v_full[j % KS], (j / KS) & 1);
       VC_TR3(trm, 0, j, 1);
-      if (more) issue_s(0, j + 1);
-      VC_TR3(trm, 0, j, 2);
-      issue_pv(0, j);
-      VC_TR3(trm, 0, j, 3);
-      if (more && ntile == 2) issue_s(1, j + 1);
-      VC_TR3(trm, 0, j, 4);
-      if (ntile == 2) issue_pv(1, j);
-      VC_TR3(trm, 0, j, 5);
+      if (LOCK) {
+        // lock-step: both tiles' S(j+1) first, then both PV(j); the two
+        // softmax groups then run their exp phases at the same time (4 warps
+        // per SM sub-partition in MUFU/FMA work instead of 2)
+        if (more) issue_s(0, j + 1);
+        VC_TR3(trm, 0, j, 2);
+        if (more && ntile == 2) issue_s(1, j + 1);
+        VC_TR3(trm, 0, j, 3);
+        issue_pv(0, j);
+        VC_TR3(trm, 0, j, 4);
+        if (ntile == 2) issue_pv(1, j);
+        VC_TR3(trm, 0, j, 5);
+      } else {
+        if (more) issue_s(0, j + 1);
+        VC_TR3(trm, 0, j, 2);
+        issue_pv(0, j);
+        VC_TR3(trm, 0, j, 3);
+        if (more && ntile == 2) issue_s(1, j + 1);
+        VC_TR3(trm, 0, j, 4);
+        if (ntile == 2) issue_pv(1, j);
+        VC_TR3(trm, 0, j, 5);
+      }
     }
   } else {
     // ===================== softmax (tile t, key half), correction, epilogue =====================
@@ -331,9 +352,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
           }
           pk[i >> 1] = ptx::bf16x2(e.x, e.y);
         }
+        if (PH && half == 0) {
+          ptx::tmem_st32(tmem + t * 256 + lane_off + CF::QCOL, pk);  // keys [0, 64) -> 32 TMEM columns
+          ptx::tmem_st_wait();
+        } else {
   #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          for (int u = 0; u < 8; ++u)
+            ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
         VC_TR3(trs, 1 + sw, j, 3);
         if (!ONES) {
           s2 = ptx::fadd2(s2, s2b);
@@ -397,34 +423,41 @@ int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const v
   const bool ones = !no_ones && p.dh < DP;
   // Q in TMEM (default) needs 16-byte aligned Q rows; VC_ATTN_QSMEM=1 keeps Q in smem
   static const bool q_smem = getenv("VC_ATTN_QSMEM") && atoi(getenv("VC_ATTN_QSMEM")) != 0;
-  const bool qt = !q_smem && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+  // P half in TMEM (default; VC_ATTN_PHALF=0 -> Q in TMEM instead, both do not fit)
+  static const bool ph = !(getenv("VC_ATTN_PHALF") && atoi(getenv("VC_ATTN_PHALF")) == 0);
+  const bool qt = !ph && !q_smem && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
+  // MMA issue order: lock-step (S_A S_B PV_A PV_B, default) or ping-pong (S_A PV_A S_B PV_B)
+  static const bool lock = !(getenv("VC_ATTN_PINGPONG") && atoi(getenv("VC_ATTN_PINGPONG")) != 0);
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-#define VC_ATTN3_CASE(PV, ON, Q)                                                                           \
-  if (poly == PV && ones == ON && qt == Q) {                                                               \
+#define VC_ATTN3_CASE(PV, ON, Q, PHV)                                                                      \
+  if (poly == PV && ones == ON && qt == Q && ph == PHV) {                                                  \
     static bool attr = false;                                                                              \
     if (!attr) {                                                                                           \
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc3_kernel<DP, PV, ON, Q>,                                   \
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc3_kernel<DP, PV, ON, Q, PHV>,                              \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));          \
       attr = true;                                                                                         \
     }                                                                                                      \
-    attn_tc3_kernel<DP, PV, ON, Q><<<grid, kThreads3, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, qb,  \
-                                                                      q_rows_per_seq, p);                  \
+    attn_tc3_kernel<DP, PV, ON, Q, PHV><<<grid, kThreads3, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, \
+                                                                           qb, q_rows_per_seq, p, lock);   \
     VC_CHECK_LAUNCH();                                                                                     \
     return VC_OK;                                                                                          \
   }
-  VC_ATTN3_CASE(0, false, false)
-  VC_ATTN3_CASE(0, true, false)
-  VC_ATTN3_CASE(4, false, false)
-  VC_ATTN3_CASE(4, true, false)
-  VC_ATTN3_CASE(2, true, false)
-  VC_ATTN3_CASE(3, true, false)
-  VC_ATTN3_CASE(0, false, true)
-  VC_ATTN3_CASE(0, true, true)
-  VC_ATTN3_CASE(4, false, true)
-  VC_ATTN3_CASE(4, true, true)
-  VC_ATTN3_CASE(2, true, true)
-  VC_ATTN3_CASE(3, true, true)
+  VC_ATTN3_CASE(0, false, false, false)
+  VC_ATTN3_CASE(0, true, false, false)
+  VC_ATTN3_CASE(4, false, false, false)
+  VC_ATTN3_CASE(4, true, false, false)
+  VC_ATTN3_CASE(2, true, false, false)
+  VC_ATTN3_CASE(3, true, false, false)
+  VC_ATTN3_CASE(0, false, true, false)
+  VC_ATTN3_CASE(0, true, true, false)
+  VC_ATTN3_CASE(4, false, true, false)
+  VC_ATTN3_CASE(4, true, true, false)
+  VC_ATTN3_CASE(2, true, true, false)
+  VC_ATTN3_CASE(3, true, true, false)
+  VC_ATTN3_CASE(4, true, false, true)
+  VC_ATTN3_CASE(3, true, false, true)
+  VC_ATTN3_CASE(4, false, false, true)
 #undef VC_ATTN3_CASE
   set_error("VC_POLY_EVERY must be 0 or 4 (2, 3 with the ones column)");
   return VC_EINVAL;
