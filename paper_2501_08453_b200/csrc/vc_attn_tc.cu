@@ -411,6 +411,7 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
       if (impl == 1) return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 2) return launch_attn_tc2<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 3) return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 7) return launch_attn_tc7<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 4) return launch_attn_tc4<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 5) return launch_attn_tc5<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       return launch_attn_tc6<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
@@ -418,6 +419,7 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
       if (impl == 1) return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 2) return launch_attn_tc2<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 3) return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      if (impl == 7) return launch_attn_tc7<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 4) return launch_attn_tc4<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 5) return launch_attn_tc5<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       return launch_attn_tc6<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);

@@ -53,6 +53,11 @@ template <int DP>
 int launch_attn_tc6(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
                     int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
 
+// CTA-pair (cta_group::2) variant of tc3 (vc_attn_tc7.cu).
+template <int DP>
+int launch_attn_tc7(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
+
 // Padded head dim the tensor-core kernel uses for dh (0: unsupported).
 int attn_tc_head_pad(int dh);
 
