@@ -38,26 +38,6 @@ template <int DP>
 int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
                     int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
 
-// Q and P resident in TMEM (vc_attn_tc4.cu): the default for DP <= 80.
-template <int DP>
-int launch_attn_tc4(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
-
-// 64-key blocks, S double-buffered in TMEM, Q/P in TMEM (vc_attn_tc5.cu): the default.
-template <int DP>
-int launch_attn_tc5(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
-
-// One 128-query tile, S double-buffered, 4 softmax warps per row (vc_attn_tc6.cu).
-template <int DP>
-int launch_attn_tc6(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
-
-// CTA-pair (cta_group::2) variant of tc3 (vc_attn_tc7.cu).
-template <int DP>
-int launch_attn_tc7(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
-
 // Padded head dim the tensor-core kernel uses for dh (0: unsupported).
 int attn_tc_head_pad(int dh);
 

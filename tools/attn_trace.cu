@@ -16,9 +16,6 @@
 namespace vc {
 int attn_trace_read(unsigned long long* host);
 int attn_trace3_read(unsigned long long* host);
-int attn_trace4_read(unsigned long long* host);
-int attn_trace5_read(unsigned long long* host);
-int attn_trace6_read(unsigned long long* host);
 }
 
 __global__ void fill_kernel(__nv_bfloat16* x, size_t n, uint32_t seed, float amp) {
@@ -65,14 +62,11 @@ int main(int argc, char** argv) {
   const double flop = 4.0 * Lq * (double)Lk * H * dh;
   printf("# Lq %d Lk %d H %d dh %d DP %d: %.4f ms  %.1f TFLOP/s (algorithmic dh)\n", Lq, Lk, H, dh, DP, ms,
          flop / ms / 1e9);
-  const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 6;
-  const int nroles = impl == 2 ? 3 : impl == 5 ? 9 : 17;
-  const int nj = impl == 5 ? 512 : 256;
+  const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 3;
+  const int nroles = impl == 2 ? 3 : 17;
+  const int nj = 256;
   std::vector<unsigned long long> tr(17 * 512 * 8);
-  const int trc = impl == 2 ? vc::attn_trace_read(tr.data())
-                  : impl == 3 ? vc::attn_trace3_read(tr.data())
-                  : impl == 4 ? vc::attn_trace4_read(tr.data())
-                  : impl == 5 ? vc::attn_trace5_read(tr.data()) : vc::attn_trace6_read(tr.data());
+  const int trc = impl == 2 ? vc::attn_trace_read(tr.data()) : vc::attn_trace3_read(tr.data());
   if (trc == 0) {
     unsigned long long t0 = ~0ull;
     for (auto v : tr) if (v && v < t0) t0 = v;
