@@ -401,22 +401,20 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
   if (p.Lk <= 0) { set_error("attention needs at least one key"); return VC_EINVAL; }
   if (nseq > 65535 || p.H > 65535) { set_error("attention grid too large"); return VC_ENOTSUP; }
   // A/B switch for profiling (VC_ATTN_IMPL): 1 one query tile per CTA, 2 one
-  // softmax thread per row, 3 attn_tc3 (one CTA per 256 queries), else
-  // (default) attn_tc8 = tc3 made persistent.  Slower variants measured
+  // softmax thread per row, else (default) attn_tc3.  Slower variants measured
   // in round 1 (Q/P in TMEM, 64-key double-buffered S, four warps per row,
-  // CTA pairs) are in git history at 20e1484; profiles/r01/attn_study/README.md.
-  static const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 8;
+  // CTA pairs; persistent) are in git history at 20e1484 and 028589b;
+  // profiles/r01/attn_study/README.md.
+  static const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 3;
   switch (DP) {
     case 64:
       if (impl == 1) return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 2) return launch_attn_tc2<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      if (impl == 3) return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      return launch_attn_tc8<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 80:
       if (impl == 1) return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
       if (impl == 2) return launch_attn_tc2<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      if (impl == 3) return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      return launch_attn_tc8<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 128: return launch_dp<128>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
   }
   set_error("tcgen05 attention: unsupported padded head dim %d", DP);
