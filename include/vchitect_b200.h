@@ -129,6 +129,20 @@ VC_API int vc_attention_f32(const float* q_dev, const float* k_dev, const float*
                      float* out_dev, int32_t sq, int32_t sk, int32_t dim,
                      int32_t heads, void* stream);
 
+/* The same attention on tcgen05 tensor cores (bf16 operands, fp32
+ * accumulation; the kernels the block forward runs), plus the deduplicated-
+ * text form of the full-sequence branch: the first n_weighted keys carry a
+ * multiplicity key_weight (logit + log key_weight), e.g. the F identical
+ * anchored prompt copies (model.py:257) as one key each with weight F.
+ * Head dims up to 128 (padded to 64 / 80 / 128). Device workspace of
+ * vc_attention_bf16_workspace_bytes() bytes. bf16 parity class (2e-2). */
+VC_API size_t vc_attention_bf16_workspace_bytes(int32_t sq, int32_t sk, int32_t dim,
+                                                int32_t heads);
+VC_API int vc_attention_bf16(const float* q_dev, const float* k_dev, const float* v_dev,
+                             float* out_dev, int32_t sq, int32_t sk, int32_t dim,
+                             int32_t heads, int32_t n_weighted, float key_weight,
+                             void* workspace_dev, size_t workspace_bytes, void* stream);
+
 /* LayerNorm without affine, model.py:89-92 (biased var, eps 1e-5):
  * rows x [rows][D] fp32 -> out fp32. */
 VC_API int vc_layer_norm_f32(const float* x_dev, float* out_dev, int64_t rows,

@@ -46,6 +46,8 @@ SIGNATURES = {
     "vc_block_forward_host_batched": (C.c_int, [_S, _p, _i32, C.POINTER(C.c_void_p), _p,
                                                 C.POINTER(C.c_void_p), _p, _sz, _p, _p, _p]),
     "vc_attention_f32": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _i32, _i32, _p]),
+    "vc_attention_bf16_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
+    "vc_attention_bf16": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _i32, _i32, _i32, C.c_float, _p, _sz, _p]),
     "vc_layer_norm_f32": (C.c_int, [_p, _p, _i64, _i32, _p]),
     "vc_embed_frames": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _d, _p]),
     "vc_unembed_frames": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _i32, _p]),

@@ -1,0 +1,114 @@
+"""Kernel-level parity of the tensor-core attention (vc_attention_bf16: the
+kernels the bf16 block runs) against the oracle's attention
+(numerics.py:87-107), over ragged lengths, head-dim paddings (64 / 80 / 128,
+with and without the V ones column), tiny and single-key sequences and the
+weighted (deduplicated text) keys of the full-sequence branch.  Tolerance:
+bf16 relative L2 <= 2e-2 (north star)."""
+import numpy as np
+import pytest
+
+from oracle import spsim_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def vc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2501_08453_b200 as vc
+    return vc
+
+
+def _case(seed, sq, sk, dh, H):
+    r = np.random.default_rng(seed)
+    D = dh * H
+    return r.standard_normal((sq, D)), r.standard_normal((sk, D)), r.standard_normal((sk, D))
+
+
+@pytest.mark.parametrize("sq,sk,dh,H", [
+    (1, 1, 64, 1),        # single query, single key
+    (5, 3, 66, 2),        # the 2B head dim, tiny lengths
+    (130, 129, 80, 3),    # one row / one key past a 128 tile
+    (300, 1000, 64, 4),   # DP 64 without padding (no ones column)
+    (257, 513, 128, 2),   # DP 128 (one-tile kernel)
+    (1000, 70, 48, 2),    # DP 64 with the ones column
+    (256, 300, 8, 3),     # tiny head dim
+    (600, 2500, 66, 24),  # 2B heads, many key blocks
+])
+def test_bf16_attention_matches_oracle(vc, sq, sk, dh, H):
+    q, k, v = _case(sq * 7 + sk, sq, sk, dh, H)
+    got = vc.attention(q, k, v, H, dtype="bf16")
+    ref = O.attention(q, k, v, H)
+    assert np.isfinite(got).all()
+    assert rel_l2(got, ref) <= BF16_TOL, rel_l2(got, ref)
+
+
+@pytest.mark.parametrize("sq,sk,n_w,w,dh,H", [
+    (200, 700, 256, 16.0, 66, 2),   # config-2 style: 256 text keys, F = 16
+    (64, 300, 300, 4.0, 64, 1),     # every key weighted
+    (129, 131, 1, 160.0, 80, 3),    # one weighted key, config-4 multiplicity
+])
+def test_bf16_attention_weighted_keys(vc, sq, sk, n_w, w, dh, H):
+    # the deduplicated anchored text: n_w keys with multiplicity w equal the
+    # w-fold repeated keys of the reference's sequence (model.py:247-260)
+    q, k, v = _case(n_w + sk, sq, sk, dh, H)
+    kw = np.concatenate([np.full(n_w, w), np.ones(sk - n_w)])
+    got = vc.attention(q, k, v, H, dtype="bf16", weighted_keys=(n_w, w))
+    ref = O.attention(q, k, v, H, kw)
+    assert rel_l2(got, ref) <= BF16_TOL, rel_l2(got, ref)
+    if float(w).is_integer() and w * n_w <= 4096:
+        # and the literal repetition (integer multiplicity)
+        reps = int(w)
+        k2 = np.concatenate([np.repeat(k[:n_w], reps, axis=0), k[n_w:]])
+        v2 = np.concatenate([np.repeat(v[:n_w], reps, axis=0), v[n_w:]])
+        assert rel_l2(got, O.attention(q, k2, v2, H)) <= BF16_TOL
+
+
+def test_bf16_attention_large_logits_rescale(vc):
+    # logits spanning >> 2^8 across key blocks exercise the lazy rescale path
+    q, k, v = _case(5, 256, 1024, 64, 2)
+    k[600:700] *= 6.0  # a late block with much larger logits
+    got = vc.attention(q, k, v, 2, dtype="bf16")
+    assert rel_l2(got, O.attention(q, k, v, 2)) <= BF16_TOL
+
+
+def test_bf16_attention_rejects_bad_args(vc):
+    q, k, v = _case(1, 4, 4, 64, 1)
+    with pytest.raises(ValueError):
+        vc.attention(q, k, v, 3, dtype="bf16")
+    with pytest.raises(ValueError):
+        vc.attention(q, k, v, 1, dtype="fp32", weighted_keys=(1, 2.0))
+    with pytest.raises(Exception):
+        vc.attention(q, k, v, 1, dtype="bf16", weighted_keys=(9, 2.0))  # more weighted keys than keys
+    qb, kb, vb = _case(1, 4, 4, 256, 1)
+    with pytest.raises(Exception):
+        vc.attention(qb, kb, vb, 1, dtype="bf16")  # head dim > 128 unsupported on tensor cores
+
+
+def test_bf16_attention_random_shapes(vc):
+    # property sweep (seeded, reproducible): ragged lengths x head dims x heads
+    # x optional weighted keys, each against the oracle
+    rng = np.random.default_rng(20250118)
+    for case in range(24):
+        sq, sk = int(rng.integers(1, 700)), int(rng.integers(1, 900))
+        dh = int(rng.choice([8, 16, 32, 48, 64, 66, 72, 80, 96, 128]))
+        H = int(rng.integers(1, 5))
+        q, k, v = _case(case, sq, sk, dh, H)
+        if rng.random() < 0.5:
+            n_w = int(rng.integers(0, sk + 1))
+            w = float(rng.choice([1.0, 2.0, 16.0, 160.0]))
+            kw = np.concatenate([np.full(n_w, w), np.ones(sk - n_w)])
+            got = vc.attention(q, k, v, H, dtype="bf16", weighted_keys=(n_w, w))
+            ref = O.attention(q, k, v, H, kw)
+        else:
+            got = vc.attention(q, k, v, H, dtype="bf16")
+            ref = O.attention(q, k, v, H)
+        assert rel_l2(got, ref) <= BF16_TOL, (case, sq, sk, dh, H, rel_l2(got, ref))
