@@ -330,8 +330,13 @@ constexpr size_t smem2_bytes() {
   return (size_t)stages2_for<BN>() * (BM * BK * 2 + (BN / 2) * BK * 2) + 256 + 4 * 256 * 4 + 1024;
 }
 
-template <int BN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// NP = CTA pairs per cluster.  NP = 2: the two pairs of a 4-CTA cluster
+// compute neighbouring N tiles of the same 256-row M tile and SHARE A: pair p
+// loads 64-row slice p of each CTA's 128-row A half and multicasts it to the
+// same-rank CTA of the other pair, halving the A bytes each SM pulls from L2
+// (the pair kernel was L2 -> SMEM bound: 9.3 GB of L2 reads for the QKV GEMM).
+template <int BN, int EPI, int NP>
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -351,11 +356,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   float* sbias_all = reinterpret_cast<float*>(bars + 2 * STAGES + 8);
 
   const int warp = threadIdx.x >> 5;
-  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t crank = ptx::cluster_ctarank();
+  const uint32_t rank = crank & 1;          // rank inside the CTA pair
+  const int pair = (int)(crank >> 1);       // pair inside the cluster
   const bool leader = rank == 0;
-  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int cluster = blockIdx.x / (2 * NP), nclusters = gridDim.x / (2 * NP);
   const int num_m = (int)cdiv(p.M, 2 * BM), num_n = (int)cdiv(p.N, BN);
-  const int tiles = num_m * num_n;
+  const int num_nc = (int)cdiv(num_n, NP);  // N tiles per cluster step
+  const int tiles = num_m * num_nc;
   const int kblocks = (int)cdiv(p.K, BK);
 
   if (warp == 0 && ptx::elect_one()) {
@@ -363,7 +371,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmB);
     // full[s] (leader): one arrival, the leader's expect_tx of BOTH CTAs' bytes
     // (the peer's TMA may land first: the tx count just dips below zero)
-    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    // empty[s]: one commit from every pair leader that reads this CTA's stage
+    // (NP = 2: the A slice this CTA loads also lands in the other pair)
+    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], NP); }
     // tempty (leader): one arrival per epilogue warp of both CTAs
     for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * 4); }
     ptx::fence_barrier_init();
@@ -379,12 +389,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (ptx::elect_one()) {
       int s = 0; uint32_t ph = 0;
       for (int t = cluster; t < tiles; t += nclusters) {
-        int mt, nt;
-        tile_coords(t, num_m, num_n, mt, nt);
+        int mt, ntc;
+        tile_coords(t, num_m, num_nc, mt, ntc);
+        const int nt = ntc * NP + pair;  // may be >= num_n (odd count): B is OOB, no output
         for (int kb = 0; kb < kblocks; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * (kABytes + kBBytes));
-          ptx::tma_load_2d_2sm(sA + s * kABytes, &tmA, &full[s], kb * BK, mt * 2 * BM + rank * BM);
+          if (NP == 1) {
+            ptx::tma_load_2d_2sm(sA + s * kABytes, &tmA, &full[s], kb * BK, mt * 2 * BM + rank * BM);
+          } else {  // slice `pair` (64 rows) of this rank's A half -> both pairs' same-rank CTAs
+            ptx::tma_load_2d_2sm_mc(sA + s * kABytes + pair * (BM / 2) * 128, &tmA, &full[s], kb * BK,
+                                    mt * 2 * BM + rank * BM + pair * (BM / 2), (uint16_t)((1u << rank) | (1u << (rank + 2))));
+          }
           ptx::tma_load_2d_2sm(sB + s * kBBytes, &tmB, &full[s], kb * BK, nt * BN + rank * BNH);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -411,8 +427,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint64_t bd = ptx::smem_desc(b0 + kk * 32, 0, 1024, ptx::kLayoutSW128);
               ptx::mma_bf16_ss_2sm(dtmem, ad, bd, idesc, (kb | kk) != 0);
             }
-            ptx::mma_commit_2sm_mc(&empty[s], 0x3);
-            if (kb == kblocks - 1) ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
+            ptx::mma_commit_2sm_mc(&empty[s], (uint16_t)((1u << (2 * NP)) - 1));  // every CTA that fed it
+            if (kb == kblocks - 1) ptx::mma_commit_2sm_mc(&tfull[acc], (uint16_t)(0x3u << (2 * pair)));
           }
           __syncwarp();
           if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -423,12 +439,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
     float* sbias = sbias_all + q * 256;
-    const uint32_t tempty_leader = ptx::mapa_shared(ptx::smem_u32(tempty), 0);
+    const uint32_t tempty_leader = ptx::mapa_shared(ptx::smem_u32(tempty), (uint32_t)(2 * pair));
     int local = 0;
     for (int t = cluster; t < tiles; t += nclusters, ++local) {
       const int acc = local & 1;
-      int mt, nt;
-      tile_coords(t, num_m, num_n, mt, nt);
+      int mt, ntc;
+      tile_coords(t, num_m, num_nc, mt, ntc);
+      const int nt = ntc * NP + pair;
       if (p.bias) {
         __syncwarp();
         for (int c = lane; c < BN; c += 32) {
@@ -518,18 +535,30 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams
   return VC_OK;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int NP>
 int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t st) {
   static bool attr_set = false;
   constexpr size_t smem = smem2_bytes<BN>();
   if (!attr_set) {
-    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     attr_set = true;
   }
-  const int64_t tiles = cdiv(p.M, 2 * BM) * cdiv(p.N, BN);
-  const int pairs = (int)std::min<int64_t>(tiles, num_sms() / 2);
-  gemm_tc2_kernel<BN, EPI><<<2 * pairs, kThreads, smem, st>>>(ta, tb, p);
+  const int64_t ctiles = cdiv(p.M, 2 * BM) * cdiv(cdiv(p.N, BN), NP);
+  const int clusters = (int)std::min<int64_t>(ctiles, num_sms() / (2 * NP));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(clusters * 2 * NP));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * NP;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  VC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI, NP>, ta, tb, p));
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
@@ -574,13 +603,15 @@ int make_tmap_4d_bf16(CUtensorMap* map, const void* base, const uint64_t dims_[4
   return VC_OK;
 }
 
-int gemm_tc_pick_bn(int N) {
-  // smallest padding waste among the instantiated tile widths
-  const int cands[4] = {256, 240, 176, 128};
+int gemm_tc_pick_bn(int N, int np) {
+  // smallest padded width among the instantiated tile widths, counting the
+  // idle tile of an odd N-tile count when pairs share A (np = 2); ties go to
+  // the wider tile (fewer A re-reads)
+  const int cands[6] = {256, 240, 208, 176, 160, 128};
   int best = 256;
   int64_t best_pad = INT64_MAX;
   for (int bn : cands) {
-    const int64_t pad = cdiv(N, bn) * bn - N;
+    const int64_t pad = cdiv(cdiv(N, bn), np) * np * bn - N;
     if (pad < best_pad) { best_pad = pad; best = bn; }
   }
   return best;
@@ -595,7 +626,10 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     return VC_EINVAL;
   }
   static const int bn_env = getenv("VC_GEMM_BN") ? atoi(getenv("VC_GEMM_BN")) : 0;  // tuning switch
-  if (bn == 0) bn = bn_env ? bn_env : gemm_tc_pick_bn(p.N);
+  // pairs per cluster: 1 (default) or 2 sharing A by multicast (VC_GEMM_NP=2;
+  // correct, but measured 1.63 vs 0.95 ms on the QKV GEMM: the two pairs are
+  // coupled at every k-block through the shared stage barriers)
+  static const int np_env = getenv("VC_GEMM_NP") ? atoi(getenv("VC_GEMM_NP")) : 1;
   // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
   // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
   static const bool no_mc = getenv("VC_GEMM_NO_MC") != nullptr;
@@ -604,13 +638,17 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   static const bool one_sm = getenv("VC_GEMM_1SM") != nullptr;
   const bool pair = !one_sm && epi != EPI_BF16 && cdiv(p.M, BM) >= 2;
   const int cm = (!no_mc && epi != EPI_BF16 && cdiv(p.M, BM) >= 2) ? 2 : 1;
+  if (bn == 0) bn = bn_env ? bn_env : gemm_tc_pick_bn(p.N, pair && np_env == 2 ? 2 : 1);
+  const int np = pair && np_env == 2 && cdiv(p.N, bn) >= 2 ? 2 : 1;
   CUtensorMap ta, tb;
-  VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
+  VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, np == 2 ? BM / 2 : BM, CU_TENSOR_MAP_SWIZZLE_128B));
   VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn / (pair ? 2 : cm), CU_TENSOR_MAP_SWIZZLE_128B));
 #define VC_GEMM_CASE(BNV)                                                                    \
   if (bn == BNV) {                                                                           \
-    if (pair) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32>(ta, tb, p, st)              \
-                                    : launch_impl2<BNV, EPI_QKV>(ta, tb, p, st);             \
+    if (pair && np == 2) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32, 2>(ta, tb, p, st)  \
+                                               : launch_impl2<BNV, EPI_QKV, 2>(ta, tb, p, st); \
+    if (pair) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32, 1>(ta, tb, p, st)           \
+                                    : launch_impl2<BNV, EPI_QKV, 1>(ta, tb, p, st);          \
     if (epi == EPI_BF16) return launch_impl<BNV, EPI_BF16, 1>(ta, tb, p, st);                \
     if (epi == EPI_F32)                                                                      \
       return cm == 2 ? launch_impl<BNV, EPI_F32, 2>(ta, tb, p, st)                           \
@@ -620,7 +658,9 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   }
   VC_GEMM_CASE(256)
   VC_GEMM_CASE(240)
+  VC_GEMM_CASE(208)
   VC_GEMM_CASE(176)
+  VC_GEMM_CASE(160)
   VC_GEMM_CASE(128)
 #undef VC_GEMM_CASE
   set_error("internal: no GEMM tile of width %d", bn);

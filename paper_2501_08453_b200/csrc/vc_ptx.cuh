@@ -105,6 +105,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
       : "memory");
 }
+// 2-CTA TMA load multicast to the CTAs of ctamask: each destination CTA gets
+// the box at the same smem offset; its bytes are counted on the barrier of
+// that destination's pair leader (peer bit cleared), as the pair's MMA is
+// issued there.
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem, const CUtensorMap* m, uint64_t* bar, int x, int y,
+                                                   uint16_t ctamask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(ctamask)
+      : "memory");
+}
 // 4D variant of tma_load_2d_2sm (bytes counted on the leader's mbarrier)
 __device__ __forceinline__ void tma_load_4d_2sm(void* smem, const CUtensorMap* m, uint64_t* bar, int x, int y,
                                                 int z, int w) {
