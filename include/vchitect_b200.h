@@ -205,7 +205,13 @@ VC_API int vc_gemm_bf16(const void* a_dev, int64_t lda, const void* b_dev,
  * (executor.py:187-191), and the whole prompt. The host runs
  *   stage1 -> all_to_all(send1 -> recv1) -> stage2 -> all_to_all(send2 ->
  *   recv2) -> stage3
- * with per-peer counts from vc_sp_exchange_elems (bf16 elements). bf16 only. */
+ * with per-peer counts from vc_sp_exchange_elems (bf16 elements). bf16 only.
+ * All four buffers are BRANCH-MAJOR: the first half holds the spatial
+ * branch for every peer, the second half the full-sequence branch, each half
+ * split by peer with half the per-peer count. So the exchange can run per
+ * branch and overlap compute: stage1 -> a2a#1(spatial), a2a#1(full seq) ->
+ * wait spatial -> stage2_branch(0) -> a2a#2(spatial) -> wait full seq ->
+ * stage2_branch(1) -> a2a#2(full seq) -> wait -> stage3. */
 typedef struct vc_sp_plan {
   vc_block_shape shape; /* global block shape (dtype must be VC_DTYPE_BF16) */
   int32_t nranks;       /* P: sp_size */
@@ -226,7 +232,13 @@ VC_API int vc_sp_stage1(const vc_sp_plan* plan, const void* packed_dev,
                         const float* x_local_dev, const float* prompt_dev,
                         void* send1_dev, void* workspace_dev,
                         size_t workspace_bytes, void* stream);
-/* recv1 -> head-group attention -> send2 (bf16). */
+/* One branch of stage 2 (0 spatial, 1 full sequence): that branch's half of
+ * recv1 -> head-group attention -> that branch's half of send2. */
+VC_API int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed_dev,
+                               const void* recv1_dev, void* send2_dev, int32_t branch,
+                               void* workspace_dev, size_t workspace_bytes,
+                               void* stream);
+/* recv1 -> head-group attention -> send2 (bf16); both branches. */
 VC_API int vc_sp_stage2(const vc_sp_plan* plan, const void* packed_dev,
                         const void* recv1_dev, void* send2_dev,
                         void* workspace_dev, size_t workspace_bytes,

@@ -6,7 +6,8 @@ namespace vc {
 
 // Sequence-parallel output remap (all-to-all #2 send layout, executor.py:395-412):
 // query (frame f, position l) is owned by rank r with vb[r] <= l < vb[r+1]; its
-// head-group output row goes to send2[base[r] + (branch*M_r + f*vc_r + l - vb[r]) * Dg].
+// head-group output row goes to send2[base[r] + (f*vc_r + l - vb[r]) * Dg], base[r]
+// = the (branch, r) block of the branch-major send2 [b'][r][M_r][Dg].
 struct SpOutMap {
   int32_t P;         // 0: disabled (plain output rows)
   int32_t branch;    // 0 spatial, 1 full sequence

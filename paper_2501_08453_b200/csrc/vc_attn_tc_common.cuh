@@ -132,8 +132,8 @@ __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr
       while (r + 1 < p.spo.P && p.spo.vb[r + 1] <= lpos) ++r;
       const int vc = p.spo.vb[r + 1] - p.spo.vb[r];
       const int64_t Mr = (int64_t)p.spo.F * vc;
-      orow = p.out + p.spo.base[r] + (p.spo.branch * Mr + (int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg +
-             (int64_t)h * p.dh;
+      (void)Mr;  // base[r] already points at this branch's block for rank r
+      orow = p.out + p.spo.base[r] + ((int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg + (int64_t)h * p.dh;
     }
   }
 #pragma unroll

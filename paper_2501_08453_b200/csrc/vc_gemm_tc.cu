@@ -123,11 +123,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
     const int which = (int)(r / q.SEG);
     const int64_t jj = r - which * q.SEG;
     const int hg = (int)(jj / q.DP), d0 = (int)(jj % q.DP);  // 16 | DP: the chunk is inside head hg
-    if (s.mode == 1) {  // sequence-parallel send layout
+    if (s.mode == 1) {  // sequence-parallel send layout, branch-major: [b'][g][which][m][Hg][DP]
       const int g = hg / s.Hg, hl = hg - g * s.Hg;
+      const int P = s.H / s.Hg;
       const int64_t rowlen = (int64_t)s.Hg * q.DP;
-      __nv_bfloat16* o = s.send + g * 6 * s.send_rows * rowlen +
-                         (((b == 0 ? 0 : 3) + which) * s.send_rows + m) * rowlen + hl * q.DP + d0;
+      __nv_bfloat16* o = s.send + ((int64_t)(b == 0 ? 0 : 1) * P + g) * 3 * s.send_rows * rowlen +
+                         (which * s.send_rows + m) * rowlen + hl * q.DP + d0;
       uint4 a, c;
       a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);
       a.z = pack_bf16x2(v[4], v[5]); a.w = pack_bf16x2(v[6], v[7]);

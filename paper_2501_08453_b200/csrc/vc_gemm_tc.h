@@ -27,8 +27,9 @@ struct QkvScatter {
   BranchOut sp, fs;
   __nv_bfloat16* tm;  // temporal branch, plain [row][3D]
   // mode 1 (sequence-parallel send): spatial / full-seq Q, K, V of local row m
-  // and head h go to send[g][b'][which][m][h % Hg][DP], g = h / Hg (head group
-  // owner), b' = 0 spatial / 1 full sequence; all-to-all #1 of executor.py:344.
+  // and head h go to send[b'][g][which][m][h % Hg][DP], g = h / Hg (head group
+  // owner), b' = 0 spatial / 1 full sequence (branch-major, so each branch's
+  // all-to-all #1 (executor.py:344) can go on its own); P = H / Hg.
   int32_t mode;
   int32_t Hg;
   int64_t send_rows;  // local rows M_r

@@ -37,8 +37,11 @@ struct Sp {
   int64_t F, Lv, Lt, D, H, dh, Nv, P, rank, Hg, Dg, DP, Lv_ld, Lk_ld;
   int32_t vb[17];
   int64_t M[16];       // local rows F*vc_r per rank
-  int64_t s1_off[17];  // element offsets of per-peer blocks: recv1 (by source rank)
-  int64_t s2_off[17];  // send2 (by destination rank)
+  // exchange buffers are branch-major: [b'][peer][...]; offsets of the
+  // per-peer blocks inside one branch half, and the half sizes
+  int64_t s1_off[17];  // recv1 (by source rank): 3 * M_r * Hg * DP each
+  int64_t s2_off[17];  // send2 (by destination rank): M_r * Dg each
+  int64_t half1, half2;
   QkvPad pad;
 };
 
@@ -73,9 +76,11 @@ int sp_make(const vc_sp_plan* pl, Sp* o, bool gather = false) {
   x.s1_off[0] = 0; x.s2_off[0] = 0;
   for (int r = 0; r < P; ++r) {
     x.M[r] = x.F * (x.vb[r + 1] - x.vb[r]);
-    x.s1_off[r + 1] = x.s1_off[r] + 6 * x.M[r] * x.Hg * x.DP;
-    x.s2_off[r + 1] = x.s2_off[r] + 2 * x.M[r] * x.Dg;
+    x.s1_off[r + 1] = x.s1_off[r] + 3 * x.M[r] * x.Hg * x.DP;
+    x.s2_off[r + 1] = x.s2_off[r] + x.M[r] * x.Dg;
   }
+  x.half1 = x.s1_off[P];
+  x.half2 = x.s2_off[P];
   return VC_OK;
 }
 
@@ -113,17 +118,18 @@ PackedPtrs packed_ptrs(const Sp& x, const void* packed) {
 }
 
 struct UnpackArgs {
-  const __nv_bfloat16* recv;
+  const __nv_bfloat16* recv;  // this branch's half of recv1: [r][which][M_r][Hg][DP]
   int32_t P, F, Lv, Lt, Hg, DP;
+  int32_t branch;  // 0 spatial, 1 full sequence
   int32_t vb[17];
-  int64_t off[17];  // recv1 block offsets by source rank
+  int64_t off[17];  // block offsets by source rank inside the half
   int64_t groups[17];  // prefix count of 32-row groups by source rank
   __nv_bfloat16 *qsp, *ksp, *vtsp, *qfs, *kfs, *vtfs;
   int64_t Lv_ld, Lk_ld;
 };
 
-// recv1[r][b'][which][m][Hg][DP] -> attention layouts of this head group.
-// One warp per 32 consecutive local rows of one (source, b', which) block;
+// recv1[b'][r][which][m][Hg][DP] (one branch half) -> attention layouts of this
+// head group.  One warp per 32 consecutive local rows of one (source, which) block;
 // lane = row. Q/K rows are copied whole (16-byte vectors); V is transposed
 // (lanes write consecutive keys of one head dim: coalesced).
 __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
@@ -136,12 +142,12 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
     while (w >= a.groups[r + 1]) ++r;
     const int vc = a.vb[r + 1] - a.vb[r];
     const int64_t Mr = (int64_t)a.F * vc;
-    const int64_t gpb = (Mr + 31) / 32;  // row groups per (b', which) block
+    const int64_t gpb = (Mr + 31) / 32;  // row groups per which-block
     const int64_t wl = w - a.groups[r];
-    const int blk = (int)(wl / gpb);  // b'*3 + which
-    const int64_t m = (wl - blk * gpb) * 32 + lane;
+    const int which = (int)(wl / gpb);
+    const int64_t m = (wl - which * gpb) * 32 + lane;
     if (m >= Mr) continue;
-    const int bp = blk / 3, which = blk - bp * 3;
+    const int bp = a.branch, blk = which;
     const int f = (int)(m / vc), l = a.vb[r] + (int)(m - (int64_t)f * vc);
     const __nv_bfloat16* src = a.recv + a.off[r] + ((int64_t)blk * Mr + m) * rowlen;
     const int64_t tok = (int64_t)f * a.Lv + l;  // visual token index
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
   }
 }
 
-// recv2[g][b'][m][Dg] -> acat[m][b'*2D + g*Dg + c]  (b'=0 spatial cols [0,D), b'=1 full-seq [2D,3D))
+// recv2[b'][g][m][Dg] -> acat[m][b'*2D + g*Dg + c]  (b'=0 spatial cols [0,D), b'=1 full-seq [2D,3D))
 __global__ void sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv, __nv_bfloat16* __restrict__ acat,
                                   int P, int64_t Mr, int64_t Dg, int64_t D) {
   const int64_t words = Dg / 2;  // Dg even (dh even)
@@ -175,10 +181,10 @@ __global__ void sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv, __nv_b
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t wi = e % words;
-    const int64_t row = e / words;  // (g*2 + b')*Mr + m
+    const int64_t row = e / words;  // (b'*P + g)*Mr + m
     const int64_t m = row % Mr;
     const int64_t gb = row / Mr;
-    const int g = (int)(gb / 2), bp = (int)(gb % 2);
+    const int bp = (int)(gb / P), g = (int)(gb % P);
     const uint32_t v = reinterpret_cast<const uint32_t*>(recv + row * Dg)[wi];
     reinterpret_cast<uint32_t*>(acat + m * 3 * D + bp * 2 * D + (int64_t)g * Dg)[wi] = v;
   }
@@ -362,12 +368,13 @@ int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loca
   return VC_OK;
 }
 
-int vc_sp_stage2(const vc_sp_plan* plan, const void* packed, const void* recv1, void* send2, void* ws,
-                 size_t ws_bytes, void* stream) {
+int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed, const void* recv1, void* send2, int branch,
+                        void* ws, size_t ws_bytes, void* stream) {
   Sp x;
   VC_TRY(sp_make(plan, &x));
   const SpWs w = sp_ws(x);
   if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
+  if (branch < 0 || branch > 1) { set_error("branch must be 0 (spatial) or 1 (full sequence)"); return VC_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   char* W = (char*)ws;
   typedef __nv_bfloat16 bf;
@@ -378,21 +385,22 @@ int vc_sp_stage2(const vc_sp_plan* plan, const void* packed, const void* recv1, 
   BranchOut fs{(bf*)(W + w.qfs), (bf*)(W + w.kfs), (bf*)(W + w.vtfs), x.Lk_ld};
   {
     UnpackArgs a{};
-    a.recv = (const bf*)recv1; a.P = (int)x.P; a.F = (int)x.F; a.Lv = (int)x.Lv; a.Lt = (int)x.Lt;
-    a.Hg = (int)x.Hg; a.DP = (int)x.DP;
+    a.recv = (const bf*)recv1 + branch * x.half1;
+    a.P = (int)x.P; a.F = (int)x.F; a.Lv = (int)x.Lv; a.Lt = (int)x.Lt;
+    a.Hg = (int)x.Hg; a.DP = (int)x.DP; a.branch = branch;
     a.groups[0] = 0;
     for (int r = 0; r <= x.P; ++r) { a.vb[r] = x.vb[r]; a.off[r] = x.s1_off[r]; }
-    for (int r = 0; r < x.P; ++r) a.groups[r + 1] = a.groups[r] + 6 * cdiv(x.M[r], 32);
+    for (int r = 0; r < x.P; ++r) a.groups[r + 1] = a.groups[r] + 3 * cdiv(x.M[r], 32);
     a.qsp = sp.q; a.ksp = sp.k; a.vtsp = sp.vt; a.qfs = fs.q; a.kfs = fs.k; a.vtfs = fs.vt;
     a.Lv_ld = x.Lv_ld; a.Lk_ld = x.Lk_ld;
     const int64_t warps = a.groups[x.P];
     const int blocks = (int)std::min<int64_t>(cdiv(warps, 8), 148 * 8);
     if (blocks > 0) sp_unpack1_kernel<<<blocks, 256, 0, st>>>(a);
     VC_CHECK_LAUNCH();
-    profile_mark(st, "sp_unpack1");
+    profile_mark(st, branch == 0 ? "sp_unpack1_spatial" : "sp_unpack1_fullseq");
   }
   const int g = (int)x.rank;
-  if (x.Lt > 0) {  // text K, V of this head group from the local prompt copy
+  if (branch == 1 && x.Lt > 0) {  // text K, V of this head group from the local prompt copy
     for (int part = 0; part < 2; ++part) {
       const int64_t n0 = x.pad.fs_base() + (1 + part) * x.pad.SEG + (int64_t)g * x.Hg * x.DP;
       GemmTcParams gp{};
@@ -405,23 +413,27 @@ int vc_sp_stage2(const vc_sp_plan* plan, const void* packed, const void* recv1, 
     profile_mark(st, "sp_text_kv_gemm");
   }
   const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)x.dh));
-  for (int branch = 0; branch < 2; ++branch) {
-    AttnTcParams a{};
-    a.H = (int)x.Hg; a.dh = (int)x.dh; a.scale_log2 = scale_log2;
-    a.out = (bf*)send2; a.ld_out = 0; a.col_off = 0; a.out_seq_rows = 0;
-    a.spo.P = (int)x.P; a.spo.branch = branch; a.spo.F = (int)x.F; a.spo.Lv = (int)x.Lv; a.spo.Dg = x.Dg;
-    for (int r = 0; r <= x.P; ++r) { a.spo.vb[r] = x.vb[r]; a.spo.base[r] = x.s2_off[r]; }
-    if (branch == 0) {
-      a.Lq = (int)x.Lv; a.Lk = (int)x.Lv; a.n_bias = 0; a.bias_log2 = 0.f;
-      VC_TRY(launch_attn_tc(a, sp.q, sp.k, sp.vt, (int)x.F, x.Lv, x.Lv, x.Lv_ld, (int)x.DP, st));
-      profile_mark(st, "sp_attn_spatial");
-    } else {
-      a.Lq = (int)x.Nv; a.Lk = (int)(x.Lt + x.Nv); a.n_bias = (int)x.Lt; a.bias_log2 = (float)log2((double)x.F);
-      VC_TRY(launch_attn_tc(a, fs.q, fs.k, fs.vt, 1, x.Nv, x.Lt + x.Nv, x.Lk_ld, (int)x.DP, st));
-      profile_mark(st, "sp_attn_fullseq");
-    }
+  AttnTcParams a{};
+  a.H = (int)x.Hg; a.dh = (int)x.dh; a.scale_log2 = scale_log2;
+  a.out = (bf*)send2; a.ld_out = 0; a.col_off = 0; a.out_seq_rows = 0;
+  a.spo.P = (int)x.P; a.spo.branch = branch; a.spo.F = (int)x.F; a.spo.Lv = (int)x.Lv; a.spo.Dg = x.Dg;
+  for (int r = 0; r <= x.P; ++r) { a.spo.vb[r] = x.vb[r]; a.spo.base[r] = branch * x.half2 + x.s2_off[r]; }
+  if (branch == 0) {
+    a.Lq = (int)x.Lv; a.Lk = (int)x.Lv; a.n_bias = 0; a.bias_log2 = 0.f;
+    VC_TRY(launch_attn_tc(a, sp.q, sp.k, sp.vt, (int)x.F, x.Lv, x.Lv, x.Lv_ld, (int)x.DP, st));
+    profile_mark(st, "sp_attn_spatial");
+  } else {
+    a.Lq = (int)x.Nv; a.Lk = (int)(x.Lt + x.Nv); a.n_bias = (int)x.Lt; a.bias_log2 = (float)log2((double)x.F);
+    VC_TRY(launch_attn_tc(a, fs.q, fs.k, fs.vt, 1, x.Nv, x.Lt + x.Nv, x.Lk_ld, (int)x.DP, st));
+    profile_mark(st, "sp_attn_fullseq");
   }
   return VC_OK;
+}
+
+int vc_sp_stage2(const vc_sp_plan* plan, const void* packed, const void* recv1, void* send2, void* ws,
+                 size_t ws_bytes, void* stream) {
+  VC_TRY(vc_sp_stage2_branch(plan, packed, recv1, send2, 0, ws, ws_bytes, stream));
+  return vc_sp_stage2_branch(plan, packed, recv1, send2, 1, ws, ws_bytes, stream);
 }
 
 int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, const float* x_local,

@@ -79,7 +79,9 @@ def check_plan(frames, visual_len, heads, p):
 def exchange_counts(frames, visual_len, heads, dim, p, rank, head_pad):
     """Per-peer element counts of the two all-to-alls (bf16 elements):
     send1/recv1 carry q,k,v of 2 branches for H/P heads (head dim padded to
-    head_pad); send2/recv2 carry 2 branches' attention outputs (H/P * dh)."""
+    head_pad); send2/recv2 carry 2 branches' attention outputs (H/P * dh).
+    The buffers are branch-major (vc_sp.cu): each branch is one half, split by
+    peer with half these counts (branch_counts)."""
     vb = contiguous_bounds(visual_len, p)
     M = [frames * (vb[r + 1] - vb[r]) for r in range(p)]
     hg, dg = heads // p, dim // p
@@ -89,6 +91,11 @@ def exchange_counts(frames, visual_len, heads, dim, p, rank, head_pad):
         "send2": [2 * M[r] * dg for r in range(p)],
         "recv2": [2 * M[rank] * dg for _ in range(p)],
     }
+
+
+def branch_counts(counts):
+    """Per-peer counts of ONE branch's exchange (half of every peer's block)."""
+    return {k: [c // 2 for c in v] for k, v in counts.items()}
 
 
 def head_pad(dh: int) -> int:
@@ -107,8 +114,11 @@ class TorchExchange:
         self.dist = dist
         self.group = group
 
-    def all_to_all(self, recv, send, recv_counts, send_counts):
-        self.dist.all_to_all_single(recv, send, recv_counts, send_counts, group=self.group)
+    def all_to_all(self, recv, send, recv_counts, send_counts, async_op=False):
+        """Returns a handle with .wait() (the current stream waits for the
+        collective; NCCL runs it on its own stream) when async_op."""
+        return self.dist.all_to_all_single(recv, send, recv_counts, send_counts, group=self.group,
+                                           async_op=async_op)
 
     def all_gather(self, gather, rank):
         """In place: gather is [P * slot]; this rank's slot is already filled."""
@@ -165,11 +175,17 @@ class SPBlock:
                                     _lib.ptr(prompt) if self.Lt else C.c_void_p(0), _lib.ptr(self.send1),
                                     _lib.ptr(self.ws), self.ws_bytes, _lib.stream_ptr(self.torch)), "sp stage1")
 
-    def stage2(self):
+    def stage2(self, branch=None):
+        """Both branches, or one (0 spatial / 1 full sequence)."""
         lib = _lib.load()
-        _lib.check(lib.vc_sp_stage2(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(self.recv1),
-                                    _lib.ptr(self.send2), _lib.ptr(self.ws), self.ws_bytes,
-                                    _lib.stream_ptr(self.torch)), "sp stage2")
+        if branch is None:
+            _lib.check(lib.vc_sp_stage2(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(self.recv1),
+                                        _lib.ptr(self.send2), _lib.ptr(self.ws), self.ws_bytes,
+                                        _lib.stream_ptr(self.torch)), "sp stage2")
+        else:
+            _lib.check(lib.vc_sp_stage2_branch(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(self.recv1),
+                                               _lib.ptr(self.send2), int(branch), _lib.ptr(self.ws), self.ws_bytes,
+                                               _lib.stream_ptr(self.torch)), "sp stage2")
 
     def stage3(self, x_local, out_local, add_residual=False):
         lib = _lib.load()
@@ -183,14 +199,36 @@ class SPBlock:
         return run_stages(self, x_local, prompt, out_local, exchange, add_residual)
 
 
+def _half(buf, b):
+    n = buf.numel() // 2
+    return buf[b * n:(b + 1) * n]
+
+
 def run_stages(stages, x_local, prompt, out_local, exchange, add_residual=False):
-    """The rank-local schedule: stage1 -> a2a #1 -> stage2 -> a2a #2 -> stage3.
-    `stages` provides stage1/2/3, the four exchange buffers and per-peer
-    counts (SPBlock on the GPU; a numpy stand-in in the CPU gloo test)."""
+    """The rank-local schedule with the exchange split by branch (the buffers
+    are branch-major) so it overlaps compute:
+
+      stage1 -> a2a#1 spatial, a2a#1 full-seq (async, NCCL stream)
+      wait spatial   -> stage2 spatial  -> a2a#2 spatial (async)
+      wait full-seq  -> stage2 full-seq -> a2a#2 full-seq (async)
+      wait both      -> stage3
+
+    so the full-sequence q/k/v travel while the spatial attention runs and
+    the spatial outputs travel while the full-sequence attention runs.
+    `stages` provides stage1/2/3, the four exchange buffers and per-peer counts
+    (SPBlock on the GPU; a numpy stand-in in the CPU gloo test)."""
+    bc = branch_counts(stages.counts)
     stages.stage1(x_local, prompt)
-    exchange.all_to_all(stages.recv1, stages.send1, stages.counts["recv1"], stages.counts["send1"])
-    stages.stage2()
-    exchange.all_to_all(stages.recv2, stages.send2, stages.counts["recv2"], stages.counts["send2"])
+    h1 = [exchange.all_to_all(_half(stages.recv1, b), _half(stages.send1, b), bc["recv1"], bc["send1"],
+                              async_op=True) for b in (0, 1)]
+    h2 = []
+    for b in (0, 1):
+        h1[b].wait()
+        stages.stage2(b)
+        h2.append(exchange.all_to_all(_half(stages.recv2, b), _half(stages.send2, b), bc["recv2"], bc["send2"],
+                                      async_op=True))
+    for h in h2:
+        h.wait()
     stages.stage3(x_local, out_local, add_residual)
     return out_local
 
@@ -292,13 +330,16 @@ class EmulatedRanks:
         self.vb = self.blocks[0].vb
 
     def _exchange(self, send_name, recv_name):
-        for g in range(self.P):
-            pieces = []
-            for r in range(self.P):
-                b = self.blocks[r]
-                off = sum(b.counts[send_name][:g])
-                pieces.append(getattr(b, send_name)[off:off + b.counts[send_name][g]])
-            self.torch.cat(pieces, out=getattr(self.blocks[g], recv_name))
+        # branch-major buffers: one all-to-all per branch half
+        for br in (0, 1):
+            for g in range(self.P):
+                pieces = []
+                for r in range(self.P):
+                    b = self.blocks[r]
+                    cnt = [c // 2 for c in b.counts[send_name]]
+                    off = sum(cnt[:g])
+                    pieces.append(_half(getattr(b, send_name), br)[off:off + cnt[g]])
+                self.torch.cat(pieces, out=_half(getattr(self.blocks[g], recv_name), br))
 
     def block_forward(self, xs, prompt, outs, add_residual=False, device_block=None):
         """xs / outs: per-rank [F, vc_r, D] fp32 (outs may alias xs)."""

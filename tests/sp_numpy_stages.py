@@ -2,10 +2,12 @@
 rank-local CUDA stages of the sequence-parallel block forward, using the
 same exchange buffer layouts as paper_2501_08453_b200/csrc/vc_sp.cu:
 
-  send1 (rank r) [g][b'][which][m][Hg][DP]   b' = 0 spatial, 1 full sequence
-  recv1 (rank g) [r][b'][which][M_r][Hg][DP]
-  send2 (rank g) [r][b'][M_r][Dg]
-  recv2 (rank r) [g][b'][M_r][Dg]
+  send1 (rank r) [b'][g][which][m][Hg][DP]   b' = 0 spatial, 1 full sequence
+  recv1 (rank g) [b'][r][which][M_r][Hg][DP]
+  send2 (rank g) [b'][r][M_r][Dg]
+  recv2 (rank r) [b'][g][M_r][Dg]
+
+(branch-major, so the product's driver runs one all-to-all per branch)
 
 so the real torch.distributed all_to_all_single (gloo here, NCCL on the GPU
 box) is exercised with the exact per-peer counts of the product
@@ -37,45 +39,45 @@ class NumpyStages:
         vc = xl.shape[1]
         rows = xl.reshape(-1, D)
         Mr = rows.shape[0]
-        s1 = self.send1.numpy().reshape(self.P, 2, 3, Mr, Hg, DP)
+        s1 = self.send1.numpy().reshape(2, self.P, 3, Mr, Hg, DP)
         for bp, params in enumerate((self.block.spatial, self.block.fullseq)):
             for which, t in enumerate(O.branch_qkv(params, rows)):
                 th = t.reshape(Mr, self.H, dh)
                 for g in range(self.P):
-                    s1[g, bp, which, :, :, :dh] = th[:, g * Hg:(g + 1) * Hg]
+                    s1[bp, g, which, :, :, :dh] = th[:, g * Hg:(g + 1) * Hg]
         q, k, v = O.branch_qkv(self.block.temporal, rows)
         tr = lambda a: a.reshape(F, vc, D).transpose(1, 0, 2)  # noqa: E731  [vc, F, D]
         self.a_tm = O.attention(tr(q), tr(k), tr(v), self.H).transpose(1, 0, 2).reshape(Mr, D)
         self.prompt = prompt.numpy()
 
-    # stage 2: full sequences for this head group -> outputs by row owner
-    def stage2(self):
+    # stage 2 (one branch): full sequences for this head group -> outputs by row owner
+    def stage2(self, branch):
         F, Lv, Lt, Hg, DP, dh, P = self.F, self.Lv, self.Lt, self.Hg, self.DP, self.dh, self.P
         g = self.rank
         Nv = F * Lv
-        full = np.zeros((2, 3, F, Lv, Hg * dh))
-        off = 0
+        full = np.zeros((3, F, Lv, Hg * dh))
         r1 = self.recv1.numpy()
+        off = branch * (r1.size // 2)
         for r in range(P):
             vc, Mr = self.vb[r + 1] - self.vb[r], self.M[r]
-            blk = r1[off:off + 6 * Mr * Hg * DP].reshape(2, 3, F, vc, Hg, DP)[..., :dh]
-            full[:, :, :, self.vb[r]:self.vb[r + 1]] = blk.reshape(2, 3, F, vc, Hg * dh)
-            off += 6 * Mr * Hg * DP
-        out_sp = O.attention(full[0, 0], full[0, 1], full[0, 2], Hg)            # [F, Lv, Hg*dh]
-        _, kt, vt = O.branch_qkv(self.block.fullseq, self.prompt)
-        cols = slice(g * Hg * dh, (g + 1) * Hg * dh)
-        K = np.concatenate([kt[:, cols], full[1, 1].reshape(Nv, -1)])
-        V = np.concatenate([vt[:, cols], full[1, 2].reshape(Nv, -1)])
-        w = np.concatenate([np.full(Lt, float(F)), np.ones(Nv)])
-        out_fs = O.attention(full[1, 0].reshape(Nv, -1), K, V, Hg, w).reshape(F, Lv, -1)
+            blk = r1[off:off + 3 * Mr * Hg * DP].reshape(3, F, vc, Hg, DP)[..., :dh]
+            full[:, :, self.vb[r]:self.vb[r + 1]] = blk.reshape(3, F, vc, Hg * dh)
+            off += 3 * Mr * Hg * DP
+        if branch == 0:
+            out = O.attention(full[0], full[1], full[2], Hg)            # [F, Lv, Hg*dh]
+        else:
+            _, kt, vt = O.branch_qkv(self.block.fullseq, self.prompt)
+            cols = slice(g * Hg * dh, (g + 1) * Hg * dh)
+            K = np.concatenate([kt[:, cols], full[1].reshape(Nv, -1)])
+            V = np.concatenate([vt[:, cols], full[2].reshape(Nv, -1)])
+            w = np.concatenate([np.full(Lt, float(F)), np.ones(Nv)])
+            out = O.attention(full[0].reshape(Nv, -1), K, V, Hg, w).reshape(F, Lv, -1)
         s2 = self.send2.numpy()
-        off = 0
+        off = branch * (s2.size // 2)
         for r in range(P):
             Mr = self.M[r]
-            blk = s2[off:off + 2 * Mr * self.Dg].reshape(2, F, -1, self.Dg)
-            blk[0] = out_sp[:, self.vb[r]:self.vb[r + 1]]
-            blk[1] = out_fs[:, self.vb[r]:self.vb[r + 1]]
-            off += 2 * Mr * self.Dg
+            s2[off:off + Mr * self.Dg].reshape(F, -1, self.Dg)[:] = out[:, self.vb[r]:self.vb[r + 1]]
+            off += Mr * self.Dg
 
     # stage 3: gather head-group columns, O projection (+ residual)
     def stage3(self, x_local, out_local, add_residual=False):
@@ -83,10 +85,10 @@ class NumpyStages:
         Mr = self.M[self.rank]
         acat = np.zeros((Mr, 3 * D))
         acat[:, D:2 * D] = self.a_tm
-        r2 = self.recv2.numpy().reshape(P, 2, Mr, Dg)
+        r2 = self.recv2.numpy().reshape(2, P, Mr, Dg)
         for g in range(P):
-            acat[:, g * Dg:(g + 1) * Dg] = r2[g, 0]
-            acat[:, 2 * D + g * Dg:2 * D + (g + 1) * Dg] = r2[g, 1]
+            acat[:, g * Dg:(g + 1) * Dg] = r2[0, g]
+            acat[:, 2 * D + g * Dg:2 * D + (g + 1) * Dg] = r2[1, g]
         W = np.concatenate([self.block.spatial.wo, self.block.temporal.wo, self.block.fullseq.wo])
         y = (acat @ W).reshape(x_local.shape)
         if add_residual:
