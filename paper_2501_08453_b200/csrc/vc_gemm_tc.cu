@@ -628,8 +628,10 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   }
   static const int bn_env = getenv("VC_GEMM_BN") ? atoi(getenv("VC_GEMM_BN")) : 0;  // tuning switch
   // pairs per cluster: 1 (default) or 2 sharing A by multicast (VC_GEMM_NP=2;
-  // correct, but measured 1.63 vs 0.95 ms on the QKV GEMM: the two pairs are
-  // coupled at every k-block through the shared stage barriers)
+  // correct, but measured 1.59-1.63 vs 0.93 ms on the QKV GEMM — and equally
+  // slow with the multicast replaced by plain per-CTA loads, so the cost is
+  // the 4-CTA cluster itself (tensor-pipe-active cycles grow 1.7x for the same
+  // MMAs), not the shared A)
   static const int np_env = getenv("VC_GEMM_NP") ? atoi(getenv("VC_GEMM_NP")) : 1;
   // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
   // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
