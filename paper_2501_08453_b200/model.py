@@ -24,6 +24,7 @@ changes, so in-place mutation is always seen.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import math
 from dataclasses import dataclass, field
 
@@ -162,10 +163,13 @@ def device_block(torch, block: BlockParams, heads: int, dtype: str) -> DeviceBlo
     key = (id(block), heads, dtype)
     fp = _fingerprint([a for br in block.branches() for a in br.arrays()])
     hit = _BLOCK_CACHE.get(key)
-    if hit is not None and hit[0] is block and hit[1].fingerprint == fp:
+    if hit is not None and hit[0]() is block and hit[1].fingerprint == fp:
         return hit[1]
     db = DeviceBlock(torch, block, heads, dtype)
-    _BLOCK_CACHE[key] = (block, db)
+    # weak reference: the cache must not keep a BlockParams (and its device
+    # weights) alive; the entry is dropped when the block is collected
+    _BLOCK_CACHE[key] = (weakref.ref(block), db)
+    weakref.finalize(block, _BLOCK_CACHE.pop, key, None)
     return db
 
 

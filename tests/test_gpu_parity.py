@@ -95,14 +95,15 @@ def test_block_bf16_matches_reference(vc, case):
 
 def test_text_anchoring_ignores_later_frames(vc):
     # reference tests/test_model.py:152-163: garbage in text[1:] changes nothing
-    blk, x, prompt = block_case(vc, "blk_small", 3, 5, 2, 12)
-    clean = vc.anchor_text(prompt, 3)
-    dirty = clean.copy()
-    dirty[1:] = vc.SeededRng(5).normal((2, 2, 12)) * 100
-    for dt in ("fp32", "bf16") if False else ("fp32",):
+    # (fp32 on a 12-dim block; bf16 needs dim % 8 == 0, so a 64-dim one)
+    for name, D, dt in (("blk_small", 12, "fp32"), ("anchor_bf16", 64, "bf16")):
+        blk, x, prompt = block_case(vc, name, 3, 5, 2, D)
+        clean = vc.anchor_text(prompt, 3)
+        dirty = clean.copy()
+        dirty[1:] = vc.SeededRng(5).normal((2, 2, D)) * 100
         a = vc.full_sequence_attention(blk.fullseq, clean, x, 4, dtype=dt)
         b = vc.full_sequence_attention(blk.fullseq, dirty, x, 4, dtype=dt)
-        assert np.array_equal(a, b)
+        assert np.array_equal(a, b), dt
 
 
 def test_spatial_frames_independent(vc):
@@ -174,6 +175,22 @@ def test_weight_mutation_is_seen(vc):
     model.blocks[0].fullseq.wo[:] = 0.0
     c = model.forward(lat, 37, prompt)
     assert not np.allclose(c, b)
+
+
+def test_device_weight_cache_does_not_keep_blocks_alive(vc):
+    # the packed-weight cache holds a weak reference: a collected BlockParams
+    # releases its device copy
+    import gc
+    import torch
+    from paper_2501_08453_b200 import model as M
+    blk = vc.BlockParams.init(vc.SeededRng(5).split(1000), 64)
+    db = M.device_block(torch, blk, 4, "bf16")
+    key = (id(blk), 4, "bf16")
+    assert M._BLOCK_CACHE[key][1] is db
+    assert M.device_block(torch, blk, 4, "bf16") is db  # unchanged weights: cached
+    del blk
+    gc.collect()
+    assert key not in M._BLOCK_CACHE
 
 
 # ---- 2B shapes (dh = 66), reduced frame counts so the fp64 oracle takes seconds ----
