@@ -268,3 +268,28 @@ def test_temporal_branch_long_clips(vc, F, Lv, D, H):
     ref = O.temporal_branch(O.BranchParams(*p.arrays()), x, H)
     assert normwise(vc.temporal_branch(p, x, H, dtype="fp32"), ref) <= FP32_TOL
     assert rel_l2(vc.temporal_branch(p, x, H, dtype="bf16"), ref) <= BF16_TOL
+
+
+def test_block_random_shapes_sweep(vc):
+    # seeded sweep over block geometries (frames, visual / text lengths incl.
+    # zero text, dims, heads) against the oracle, both precisions; bf16 where
+    # its layout constraints hold (dim % 8 == 0, head dim <= 128)
+    rng = np.random.default_rng(2501_08453)
+    for case in range(16):
+        F = int(rng.integers(1, 5))
+        Lv = int(rng.integers(1, 40))
+        Lt = int(rng.choice([0, 1, 3, 16]))
+        H = int(rng.choice([1, 2, 3, 4]))
+        dh = int(rng.choice([4, 8, 16, 24, 32, 48, 66]))
+        D = H * dh
+        blk = vc.BlockParams.init(vc.SeededRng(1000 + case).split(1000), D)
+        x = rng.standard_normal((F, Lv, D))
+        prompt = rng.standard_normal((Lt, D))
+        text = vc.anchor_text(prompt, F)
+        oblk = O.BlockParams(*[O.BranchParams(*b.arrays()) for b in blk.branches()])
+        ref = O.parallel_block_forward(oblk, x, O.anchor_text(prompt, F), H)
+        got32 = vc.parallel_block_forward(blk, x, text, H, dtype="fp32")
+        assert normwise(got32, ref) <= FP32_TOL, (case, F, Lv, Lt, D, H)
+        if D % 8 == 0:
+            got16 = vc.parallel_block_forward(blk, x, text, H, dtype="bf16")
+            assert rel_l2(got16, ref) <= BF16_TOL, (case, F, Lv, Lt, D, H, rel_l2(got16, ref))
