@@ -518,9 +518,7 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams
     attr_set = true;
   }
   const int64_t ctiles = cdiv(cdiv(p.M, BM), CM) * cdiv(p.N, BN);
-  const int clusters = (int)std::min<int64_t>(ctiles, num_sms() / CM);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(clusters * CM));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -531,6 +529,17 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // persistent grid = the clusters that can be resident at once (GPC packing
+  // limits clusters of 4 well below num_SMs / 4)
+  static int resident = 0;
+  if (!resident) {
+    cfg.gridDim = dim3((unsigned)(num_sms() / CM * CM));
+    if (cudaOccupancyMaxActiveClusters(&resident, gemm_tc_kernel<BN, EPI, CM>, &cfg) != cudaSuccess || resident <= 0)
+      resident = num_sms() / CM;
+    if (getenv("VC_GEMM_DEBUG")) fprintf(stderr, "gemm_tc CM=%d: %d resident clusters\n", CM, resident);
+  }
+  const int clusters = (int)std::min<int64_t>(ctiles, resident);
+  cfg.gridDim = dim3((unsigned)(clusters * CM));
   VC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, EPI, CM>, ta, tb, p));
   VC_CHECK_LAUNCH();
   return VC_OK;
@@ -546,9 +555,7 @@ int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParam
     attr_set = true;
   }
   const int64_t ctiles = cdiv(p.M, 2 * BM) * cdiv(cdiv(p.N, BN), NP);
-  const int clusters = (int)std::min<int64_t>(ctiles, num_sms() / (2 * NP));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(clusters * 2 * NP));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -559,6 +566,16 @@ int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParam
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static int resident = 0;  // co-resident clusters (see launch_impl)
+  if (!resident) {
+    cfg.gridDim = dim3((unsigned)(num_sms() / (2 * NP) * 2 * NP));
+    if (cudaOccupancyMaxActiveClusters(&resident, gemm_tc2_kernel<BN, EPI, NP>, &cfg) != cudaSuccess ||
+        resident <= 0)
+      resident = num_sms() / (2 * NP);
+    if (getenv("VC_GEMM_DEBUG")) fprintf(stderr, "gemm_tc2 NP=%d: %d resident clusters\n", NP, resident);
+  }
+  const int clusters = (int)std::min<int64_t>(ctiles, resident);
+  cfg.gridDim = dim3((unsigned)(clusters * 2 * NP));
   VC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI, NP>, ta, tb, p));
   VC_CHECK_LAUNCH();
   return VC_OK;
@@ -627,12 +644,12 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     return VC_EINVAL;
   }
   static const int bn_env = getenv("VC_GEMM_BN") ? atoi(getenv("VC_GEMM_BN")) : 0;  // tuning switch
-  // pairs per cluster: 1 (default) or 2 sharing A by multicast (VC_GEMM_NP=2;
-  // correct, but measured 1.59-1.63 vs 0.93 ms on the QKV GEMM — and equally
-  // slow with the multicast replaced by plain per-CTA loads, so the cost is
-  // the 4-CTA cluster itself (tensor-pipe-active cycles grow 1.7x for the same
-  // MMAs), not the shared A)
-  static const int np_env = getenv("VC_GEMM_NP") ? atoi(getenv("VC_GEMM_NP")) : 1;
+  // pairs per cluster: 2 sharing A by multicast for the O GEMM (EPI_F32:
+  // 0.245 vs 0.264 ms), 1 for the QKV GEMM (0.94 vs 0.98: only 33 clusters of
+  // 4 fit at once, 132 of 148 SMs, which eats the L2 saving); VC_GEMM_NP
+  // overrides.  (Before the grid was sized with cudaOccupancyMaxActiveClusters
+  // the 4-CTA clusters ran in two waves and looked 1.7x slower.)
+  static const int np_env = getenv("VC_GEMM_NP") ? atoi(getenv("VC_GEMM_NP")) : 0;
   // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
   // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
   static const bool no_mc = getenv("VC_GEMM_NO_MC") != nullptr;
@@ -640,12 +657,15 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   // selects the single-CTA kernel with B multicast (A/B switch for profiling)
   static const bool one_sm = getenv("VC_GEMM_1SM") != nullptr;
   const bool pair = !one_sm && epi != EPI_BF16 && cdiv(p.M, BM) >= 2;
-  const int cm = (!no_mc && epi != EPI_BF16 && cdiv(p.M, BM) >= 2) ? 2 : 1;
-  if (bn == 0) bn = bn_env ? bn_env : gemm_tc_pick_bn(p.N, pair && np_env == 2 ? 2 : 1);
-  const int np = pair && np_env == 2 && cdiv(p.N, bn) >= 2 ? 2 : 1;
+  static const int cm_env = getenv("VC_GEMM_CM") ? atoi(getenv("VC_GEMM_CM")) : 2;  // 1-CTA kernel cluster
+  const int cm = (!no_mc && epi != EPI_BF16 && cdiv(p.M, BM) >= 2) ? (cm_env == 4 && cdiv(p.M, BM) >= 4 ? 4 : 2) : 1;
+  const int np_want = np_env ? np_env : (epi == EPI_F32 ? 2 : 1);
+  if (bn == 0) bn = bn_env ? bn_env : gemm_tc_pick_bn(p.N, pair && np_want == 2 ? 2 : 1);
+  const int np = pair && np_want == 2 && cdiv(p.N, bn) >= 2 ? 2 : 1;
   CUtensorMap ta, tb;
   VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, np == 2 ? BM / 2 : BM, CU_TENSOR_MAP_SWIZZLE_128B));
-  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn / (pair ? 2 : cm), CU_TENSOR_MAP_SWIZZLE_128B));
+  const int cm_eff = cm == 4 && (bn / 4) % 8 != 0 ? 2 : cm;
+  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn / (pair ? 2 : cm_eff), CU_TENSOR_MAP_SWIZZLE_128B));
 #define VC_GEMM_CASE(BNV)                                                                    \
   if (bn == BNV) {                                                                           \
     if (pair && np == 2) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32, 2>(ta, tb, p, st)  \
@@ -653,10 +673,13 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     if (pair) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32, 1>(ta, tb, p, st)           \
                                     : launch_impl2<BNV, EPI_QKV, 1>(ta, tb, p, st);          \
     if (epi == EPI_BF16) return launch_impl<BNV, EPI_BF16, 1>(ta, tb, p, st);                \
+    if (cm == 4 && (BNV / 4) % 8 == 0)                                                       \
+      return epi == EPI_F32 ? launch_impl<BNV, EPI_F32, ((BNV / 4) % 8 == 0 ? 4 : 2)>(ta, tb, p, st) \
+                            : launch_impl<BNV, EPI_QKV, ((BNV / 4) % 8 == 0 ? 4 : 2)>(ta, tb, p, st); \
     if (epi == EPI_F32)                                                                      \
-      return cm == 2 ? launch_impl<BNV, EPI_F32, 2>(ta, tb, p, st)                           \
+      return cm >= 2 ? launch_impl<BNV, EPI_F32, 2>(ta, tb, p, st)                           \
                      : launch_impl<BNV, EPI_F32, 1>(ta, tb, p, st);                          \
-    return cm == 2 ? launch_impl<BNV, EPI_QKV, 2>(ta, tb, p, st)                             \
+    return cm >= 2 ? launch_impl<BNV, EPI_QKV, 2>(ta, tb, p, st)                             \
                    : launch_impl<BNV, EPI_QKV, 1>(ta, tb, p, st);                            \
   }
   VC_GEMM_CASE(256)
