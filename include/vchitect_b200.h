@@ -295,6 +295,41 @@ VC_API int vc_profile_read(double* ms_total, int32_t* calls, int32_t max_stages,
  * bench's gpu_launches accounting). */
 VC_API int vc_block_forward_launches(const vc_block_shape* shape);
 
+/* ---- north-star extensions (no reference counterpart; PARITY UNPINNED) ----
+ * BASELINE.json's north_star names pieces of the Vchitect-2.0 block that the
+ * reference spsim block (model.py:263-271) lacks (SURVEY.md §8 "a-ext"):
+ * AdaLN timestep modulation, QK-RMSNorm + 3D RoPE fused into the Q/K
+ * projection epilogue, the gated residual and the gated GELU FFN.  Their
+ * semantics are defined by oracle/vchitect_ext_oracle.py:
+ *   mod = silu(sinusoidal_embedding(t, D)) @ w_ada + b_ada   -> 6 x [D]
+ *   h = x + gate_msa * block'(LN(x) * (1 + scale_msa) + shift_msa)
+ *   y = h + gate_mlp * (gelu_tanh(n2 @ w1 + b1) @ w2 + b2),
+ *       n2 = LN(h) * (1 + scale_mlp) + shift_mlp
+ * where block' is the reference block with RMSNorm + RoPE on the spatial and
+ * full-sequence Q/K heads.  bf16 only; the reference-semantics entry points
+ * above are unchanged by any of this. */
+typedef struct vc_ext_shape {
+  vc_block_shape block;   /* dtype must be VC_DTYPE_BF16, head dim even */
+  int32_t grid_h, grid_w; /* patch grid, grid_h * grid_w == visual_len (RoPE rows / columns) */
+  int32_t ffn_dim;        /* FFN hidden width (mlp_ratio * D), multiple of 8 */
+} vc_ext_shape;
+
+/* Raw fp32 extension weights, concatenated: w_ada [D][6D], b_ada [6D],
+ * q_norm [2][dh], k_norm [2][dh] (rows: spatial, full sequence),
+ * w1 [D][ffn], b1 [ffn], w2 [ffn][D], b2 [D] (x @ W layout). */
+VC_API size_t vc_ext_raw_weight_floats(const vc_ext_shape* shape);
+VC_API size_t vc_ext_packed_weight_bytes(const vc_ext_shape* shape);
+VC_API int vc_pack_ext_weights(const vc_ext_shape* shape, const float* raw_dev, void* packed_dev,
+                               void* stream);
+VC_API size_t vc_ext_workspace_bytes(const vc_ext_shape* shape);
+/* y = extended block(visual, prompt, timestep); block_packed_dev from
+ * vc_pack_block_weights (bf16), out_dev must not alias visual_dev. */
+VC_API int vc_ext_block_forward(const vc_ext_shape* shape, const void* block_packed_dev,
+                                const void* ext_packed_dev, const float* visual_dev,
+                                const float* prompt_dev, double timestep, float* out_dev,
+                                void* workspace_dev, size_t workspace_bytes, void* stream);
+VC_API int vc_ext_block_launches(const vc_ext_shape* shape);
+
 #ifdef __cplusplus
 }
 #endif

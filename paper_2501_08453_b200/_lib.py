@@ -24,6 +24,11 @@ class BlockShape(C.Structure):
                 ("dim", C.c_int32), ("heads", C.c_int32), ("dtype", C.c_int32)]
 
 
+class ExtShape(C.Structure):
+    _fields_ = [("block", BlockShape), ("grid_h", C.c_int32), ("grid_w", C.c_int32),
+                ("ffn_dim", C.c_int32)]
+
+
 class SpPlan(C.Structure):
     _fields_ = [("shape", BlockShape), ("nranks", C.c_int32), ("rank", C.c_int32)]
 
@@ -69,6 +74,12 @@ SIGNATURES = {
     "vc_spg_slot_elems": (_i64, [C.POINTER(SpPlan)]),
     "vc_spg_stage1": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _p, _sz, _p]),
     "vc_spg_stage2": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, C.c_int, _p, _sz, _p]),
+    "vc_ext_raw_weight_floats": (_sz, [C.POINTER(ExtShape)]),
+    "vc_ext_packed_weight_bytes": (_sz, [C.POINTER(ExtShape)]),
+    "vc_pack_ext_weights": (C.c_int, [C.POINTER(ExtShape), _p, _p, _p]),
+    "vc_ext_workspace_bytes": (_sz, [C.POINTER(ExtShape)]),
+    "vc_ext_block_forward": (C.c_int, [C.POINTER(ExtShape), _p, _p, _p, _p, _d, _p, _p, _sz, _p]),
+    "vc_ext_block_launches": (C.c_int, [C.POINTER(ExtShape)]),
     "vc_profile_enable": (C.c_int, [C.c_int]),
     "vc_profile_reset": (None, []),
     "vc_profile_read": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int32, C.c_char_p, C.c_size_t]),

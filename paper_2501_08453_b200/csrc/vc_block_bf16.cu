@@ -49,11 +49,15 @@ size_t bf16_workspace_bytes(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_
   return ws_layout(F, Lv, Lt, D, H).total;
 }
 
+size_t bf16_workspace_acat_offset(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
+  return ws_layout(F, Lv, Lt, D, H).acat;
+}
+
 int bf16_launch_count(int64_t, int64_t, int64_t Lt, int64_t, int64_t) { return Lt > 0 ? 7 : 6; }
 
 int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, const void* wqkv,
                        const float* bias, const void* wo, const float* x, const float* prompt,
-                       float* out, int add_residual, char* ws, cudaStream_t st) {
+                       float* out, int add_residual, char* ws, cudaStream_t st, const ExtArgs* ext) {
   const WsBf16 wl = ws_layout(F, Lv, Lt, D, H);
   const int64_t Nv = F * Lv, dh = D / H;
   if (wl.DP == 0) { set_error("head dim %lld unsupported on the tensor-core path", (long long)dh); return VC_ENOTSUP; }
@@ -62,7 +66,8 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   bf* acat = (bf*)(ws + wl.acat);
   bf* tm = (bf*)(ws + wl.tm);
 
-  VC_TRY(launch_ln_rows<bf>(x, Nv, prompt, Lt, (int)D, xhat, st));
+  if (ext) VC_TRY(launch_ln_rows_mod(x, Nv, prompt, Lt, (int)D, ext->mod, ext->mod + D, xhat, st));
+  else VC_TRY(launch_ln_rows<bf>(x, Nv, prompt, Lt, (int)D, xhat, st));
   profile_mark(st, "ln");
 
   const QkvPad pad = qkv_pad_layout(D, H);
@@ -71,7 +76,21 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   sc.sp = BranchOut{(bf*)(ws + wl.qsp), (bf*)(ws + wl.ksp), (bf*)(ws + wl.vtsp), wl.Lv_ld};
   sc.fs = BranchOut{(bf*)(ws + wl.qfs), (bf*)(ws + wl.kfs), (bf*)(ws + wl.vtfs), wl.Lk_ld};
   sc.tm = tm;
-  {
+  const int qkv_epi = ext ? EPI_QKVN : EPI_QKV;
+  if (ext) {
+    sc.qn[0] = ext->qn[0]; sc.qn[1] = ext->qn[1]; sc.kn[0] = ext->kn[0]; sc.kn[1] = ext->kn[1];
+    sc.rope = ext->rope; sc.dh = (int)dh; sc.gw = ext->gw;
+    sc.rope_nt = ext->rope_nt; sc.rope_ny = ext->rope_ny; sc.rope_nx = ext->rope_nx;
+    sc.rope_off_y = ext->rope_off_y; sc.rope_off_x = ext->rope_off_x;
+    // two launches so each starts on a segment base (head-aligned tiles):
+    // [sp.q sp.k sp.v | tm] and [fs.q fs.k fs.v]
+    GemmTcParams g{};
+    g.M = Nv; g.N = (int)pad.fs_base(); g.K = (int)D; g.bias = bias;
+    g.qkv = sc; g.qkv.n_base = 0; g.qkv.text_rows = 0;
+    VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_QKVN, st));
+    g.N = (int)(3 * pad.SEG); g.bias = bias + pad.fs_base(); g.qkv.n_base = pad.fs_base();
+    VC_TRY(launch_gemm_tc(xhat, D, (const bf*)wqkv + pad.fs_base() * D, D, g, EPI_QKVN, st));
+  } else {
     GemmTcParams g{};
     g.M = Nv; g.N = (int)pad.Npad; g.K = (int)D; g.bias = bias;
     g.qkv = sc; g.qkv.n_base = 0; g.qkv.text_rows = 0;
@@ -83,7 +102,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     GemmTcParams g{};
     g.M = Lt; g.N = (int)(2 * pad.SEG); g.K = (int)D; g.bias = bias + n0;
     g.qkv = sc; g.qkv.n_base = n0; g.qkv.text_rows = 1;
-    VC_TRY(launch_gemm_tc(xhat + Nv * D, D, (const bf*)wqkv + n0 * D, D, g, EPI_QKV, st));
+    VC_TRY(launch_gemm_tc(xhat + Nv * D, D, (const bf*)wqkv + n0 * D, D, g, qkv_epi, st));
     profile_mark(st, "text_kv_gemm");
   }
   const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)dh));
@@ -105,6 +124,28 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_attn_tc(a, sc.fs.q, sc.fs.k, sc.fs.vt, 1, Nv, Lt + Nv, wl.Lk_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_fullseq");
+  if (ext) {  // h = x + gate_msa * (branch sum)  -> out
+    GemmTcParams g{};
+    g.M = Nv; g.N = (int)D; g.K = (int)(3 * D);
+    g.out_f32 = out; g.ldo = D; g.R = x; g.ldr = D; g.gate = ext->mod + 2 * D;
+    VC_TRY(launch_gemm_tc(acat, 3 * D, wo, 3 * D, g, EPI_F32G, st));
+    profile_mark(st, "oproj_gemm");
+    // FFN: n2 = LN(h)(1 + scale_mlp) + shift_mlp; u = gelu(n2 W1 + b1);
+    // out = h + gate_mlp * (u W2 + b2)
+    VC_TRY(launch_ln_rows_mod(out, Nv, nullptr, 0, (int)D, ext->mod + 3 * D, ext->mod + 4 * D, xhat, st));
+    profile_mark(st, "ln_mlp");
+    GemmTcParams g1{};
+    g1.M = Nv; g1.N = (int)ext->Dff; g1.K = (int)D; g1.bias = ext->b1;
+    g1.out_bf16 = ext->u; g1.ldo = ext->Dff;
+    VC_TRY(launch_gemm_tc(xhat, D, ext->w1, D, g1, EPI_GELU, st));
+    profile_mark(st, "ffn1_gemm");
+    GemmTcParams g2{};
+    g2.M = Nv; g2.N = (int)D; g2.K = (int)ext->Dff; g2.bias = ext->b2;
+    g2.out_f32 = out; g2.ldo = D; g2.R = out; g2.ldr = D; g2.gate = ext->mod + 5 * D;
+    VC_TRY(launch_gemm_tc(ext->u, ext->Dff, ext->w2, ext->Dff, g2, EPI_F32G, st));
+    profile_mark(st, "ffn2_gemm");
+    return VC_OK;
+  }
   {
     GemmTcParams g{};
     g.M = Nv; g.N = (int)D; g.K = (int)(3 * D);

@@ -58,12 +58,52 @@ __device__ __forceinline__ void qkv_rows(const QkvScatter& s, int b, int64_t m, 
 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m, int n0,
-                                               const uint32_t (&r)[16], const float* sbias) {
+                                               const uint32_t (&r)[16], const float* sbias,
+                                               const float* sgate = nullptr) {
   if (m >= p.M) return;
   float v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) + (sbias ? sbias[j] : 0.f);  // smem broadcast
-  if constexpr (EPI == EPI_F32) {
+  if constexpr (EPI == EPI_F32G) {  // R + gate * (acc + bias); gate staged in smem per tile
+    float* o = p.out_f32 + m * p.ldo + n0;
+    const float* R = p.R + m * p.ldr + n0;
+    if (n0 + 16 <= p.N && (p.ldo % 4) == 0 && (p.ldr % 4) == 0) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float4 rr = *reinterpret_cast<const float4*>(R + j);
+        float4 w;
+        w.x = fmaf(sgate[j], v[j], rr.x); w.y = fmaf(sgate[j + 1], v[j + 1], rr.y);
+        w.z = fmaf(sgate[j + 2], v[j + 2], rr.z); w.w = fmaf(sgate[j + 3], v[j + 3], rr.w);
+        *reinterpret_cast<float4*>(o + j) = w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n0 + j < p.N) o[j] = fmaf(sgate[j], v[j], R[j]);
+    }
+  } else if constexpr (EPI == EPI_GELU) {
+    __nv_bfloat16* o = p.out_bf16 + m * p.ldo + n0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {  // 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+      const float u = 0.7978845608028654f * fmaf(0.044715f * v[j], v[j] * v[j], v[j]);
+      float th;
+      asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(u));
+      v[j] = 0.5f * v[j] * (1.f + th);
+    }
+    if (n0 + 16 <= p.N && (p.ldo % 8) == 0) {
+      uint4 a, b;
+      a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);
+      a.z = pack_bf16x2(v[4], v[5]); a.w = pack_bf16x2(v[6], v[7]);
+      b.x = pack_bf16x2(v[8], v[9]); b.y = pack_bf16x2(v[10], v[11]);
+      b.z = pack_bf16x2(v[12], v[13]); b.w = pack_bf16x2(v[14], v[15]);
+      reinterpret_cast<uint4*>(o)[0] = a;
+      reinterpret_cast<uint4*>(o)[1] = b;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n0 + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else if constexpr (EPI == EPI_F32) {
     float* o = p.out_f32 + m * p.ldo + n0;
     const float* R = p.R ? p.R + m * p.ldr + n0 : nullptr;
     if (n0 + 16 <= p.N && (p.ldo % 4) == 0 && (!R || (p.ldr % 4) == 0)) {
@@ -158,6 +198,91 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
 #pragma unroll
       for (int i = 0; i < 16; ++i) o[(int64_t)i * bo.ld_key] = __float2bfloat16_rn(v[i]);
     }
+  }
+}
+
+// ---- EPI_QKVN: one head (DP columns) of one row, QK-RMSNorm + 3D RoPE ----
+// The tile is head aligned (BN % DP == 0, the launch starts at a segment
+// base), so the thread owning row m holds every column of head hg: it loads
+// the DP accumulator columns from TMEM, adds the bias, and for Q / K of the
+// spatial and full-sequence branches normalises over the dh real dims
+// (rms(u) * w, eps 1e-6), rotates the dh/2 pairs by the token's (frame, row,
+// column) angles and stores the DP-wide head row.  V and the temporal
+// columns take the plain EPI_QKV chunk path.  (oracle/vchitect_ext_oracle.py)
+template <int DP>
+__device__ __forceinline__ void qkvn_head(const GemmTcParams& p, int64_t m, int n0, uint32_t taddr,
+                                          const float* sbias) {
+  const QkvScatter& s = p.qkv;
+  const QkvPad& q = s.pad;
+  const int64_t n = n0 + s.n_base;
+  const bool tmseg = n >= 3 * q.SEG && n < q.fs_base();
+  int b = 0, which = 2, hg = 0;
+  if (!tmseg) {
+    b = n < 3 * q.SEG ? 0 : 2;
+    const int64_t r = b == 0 ? n : n - q.fs_base();
+    which = (int)(r / q.SEG);
+    hg = (int)((r - which * q.SEG) / DP);
+  }
+  uint32_t u[DP];
+#pragma unroll
+  for (int c = 0; c < DP / 16; ++c) ptx::tmem_ld16p(taddr + c * 16, u + c * 16);
+  ptx::tmem_ld_wait();
+  if (tmseg || which == 2) {  // warp-uniform: V^T / temporal columns, plain scatter
+#pragma unroll
+    for (int c = 0; c < DP / 16; ++c) {
+      if (n0 + c * 16 >= p.N) break;
+      uint32_t r[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) r[j] = u[c * 16 + j];
+      epilogue_chunk<EPI_QKV>(p, m, n0 + c * 16, r, sbias ? sbias + c * 16 : nullptr);
+    }
+    return;
+  }
+  if (m >= p.M) return;
+  float v[DP];
+  float ss4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 partial sums: short dependency chains
+#pragma unroll
+  for (int d = 0; d < DP; ++d) {
+    v[d] = __uint_as_float(u[d]) + (sbias ? sbias[d] : 0.f);
+    ss4[d & 3] = fmaf(v[d], v[d], ss4[d & 3]);  // padding columns are exact zeros (zero weights and bias)
+  }
+  const float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
+  const int bi = b == 0 ? 0 : 1;
+  const float* w = which == 0 ? s.qn[bi] : s.kn[bi];
+  const float rs = rsqrtf(ss / (float)s.dh + 1e-6f);
+#pragma unroll
+  for (int d = 0; d < DP; ++d)
+    if (d < s.dh) v[d] *= rs * __ldg(w + d);
+  int64_t qrow, krow, seq, key;
+  qkv_rows(s, b, m, qrow, krow, seq, key);
+  if (!s.text_rows) {  // visual token: (frame, row, column) rotation
+    const int64_t f = m / s.Lv, l = m - f * s.Lv;
+    const int y = (int)(l / s.gw), x = (int)(l - (int64_t)(l / s.gw) * s.gw);
+    const int nt = s.rope_nt, nty = s.rope_nt + s.rope_ny;
+    const float2* pt = s.rope + f * nt;
+    const float2* py = s.rope + s.rope_off_y + (int64_t)y * s.rope_ny - nt;
+    const float2* px = s.rope + s.rope_off_x + (int64_t)x * s.rope_nx - nty;
+#pragma unroll
+    for (int i = 0; i < DP / 2; ++i) {
+      if (2 * i < s.dh) {
+        const float2 cs = __ldg(i < nt ? pt + i : i < nty ? py + i : px + i);
+        const float a = v[2 * i], c = v[2 * i + 1];
+        v[2 * i] = a * cs.x - c * cs.y;
+        v[2 * i + 1] = fmaf(a, cs.y, c * cs.x);
+      }
+    }
+  }
+  const int h = hg - s.head_base;
+  const BranchOut& bo = b == 0 ? s.sp : s.fs;
+  const int64_t row = which == 0 ? qrow : krow;
+  if (row < 0) return;
+  uint4* o = reinterpret_cast<uint4*>((which == 0 ? bo.q : bo.k) + (row * s.H + h) * DP);
+#pragma unroll
+  for (int c = 0; c < DP / 8; ++c) {
+    uint4 a;
+    a.x = pack_bf16x2(v[8 * c], v[8 * c + 1]); a.y = pack_bf16x2(v[8 * c + 2], v[8 * c + 3]);
+    a.z = pack_bf16x2(v[8 * c + 4], v[8 * c + 5]); a.w = pack_bf16x2(v[8 * c + 6], v[8 * c + 7]);
+    o[c] = a;
   }
 }
 
@@ -326,9 +451,10 @@ template <int BN>
 constexpr int stages2_for() {
   return (216 * 1024) / (BM * BK * 2 + (BN / 2) * BK * 2) > 8 ? 8 : (216 * 1024) / (BM * BK * 2 + (BN / 2) * BK * 2);
 }
-template <int BN>
-constexpr size_t smem2_bytes() {
-  return (size_t)stages2_for<BN>() * (BM * BK * 2 + (BN / 2) * BK * 2) + 256 + 4 * 256 * 4 + 1024;
+template <int BN, int EPI>
+constexpr size_t smem2_bytes() {  // stages + barriers + bias staging (+ gate staging, EPI_F32G) + align
+  return (size_t)stages2_for<BN>() * (BM * BK * 2 + (BN / 2) * BK * 2) + 256 + 4 * 256 * 4 +
+         (EPI == EPI_F32G ? 4 * 256 * 4 : 0) + 1024;
 }
 
 // NP = CTA pairs per cluster.  NP = 2: the two pairs of a 4-CTA cluster
@@ -440,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
     float* sbias = sbias_all + q * 256;
+    float* sgate = sbias_all + 4 * 256 + q * 256;  // EPI_F32G only (smem2_bytes)
     const uint32_t tempty_leader = ptx::mapa_shared(ptx::smem_u32(tempty), (uint32_t)(2 * pair));
     int local = 0;
     for (int t = cluster; t < tiles; t += nclusters, ++local) {
@@ -455,19 +582,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ptx::fence_after_sync();
       const int64_t mrow0 = (int64_t)mt * 2 * BM + rank * BM;
       const int64_t m = mrow0 + q * 32 + lane;
+      if constexpr (EPI == EPI_F32G) {
+        __syncwarp();
+        for (int c = lane; c < BN; c += 32) {
+          const int n = nt * BN + c;
+          sgate[c] = n < p.N ? __ldg(p.gate + n) : 0.f;
+        }
+        __syncwarp();
+      }
+      if constexpr (EPI == EPI_F32 || EPI == EPI_F32G) {
+        // the residual rows do not depend on the accumulator: pull this
+        // thread's R segment into L2 while the tile's MMAs run, so the
+        // epilogue's loads hit L2 instead of paying HBM latency per chunk
+        if (p.R && m < p.M) {
+          const char* rp = reinterpret_cast<const char*>(p.R + m * p.ldr + (int64_t)nt * BN);
+          const int nb = min(BN, p.N - nt * BN) * 4;
+          for (int b = 0; b < nb; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + b));
+        }
+      }
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::fence_after_sync();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+      if constexpr ((EPI & 255) == EPI_QKVN) {  // EPI = EPI_QKVN | DP << 8: head by head
+        constexpr int EDP = EPI >> 8;
 #pragma unroll 1
-      for (int c = 0; c < BN / 16; ++c) {
-        const int n0 = nt * BN + c * 16;
-        if (n0 >= p.N || mrow0 >= p.M) break;
-        uint32_t r[16];
-        ptx::tmem_ld16(tbase + c * 16, r);
-        ptx::tmem_ld_wait();
-        epilogue_chunk<EPI>(p, m, n0, r, p.bias ? sbias + c * 16 : nullptr);
+        for (int hb = 0; hb < BN / EDP; ++hb) {
+          const int n0 = nt * BN + hb * EDP;
+          if (n0 >= p.N || mrow0 >= p.M) break;
+          qkvn_head<EDP>(p, m, n0, tbase + hb * EDP, p.bias ? sbias + hb * EDP : nullptr);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 16; ++c) {
+          const int n0 = nt * BN + c * 16;
+          if (n0 >= p.N || mrow0 >= p.M) break;
+          uint32_t r[16];
+          ptx::tmem_ld16(tbase + c * 16, r);
+          ptx::tmem_ld_wait();
+          epilogue_chunk<EPI>(p, m, n0, r, p.bias ? sbias + c * 16 : nullptr, sgate + c * 16);
+        }
       }
       ptx::fence_before_sync();
       __syncwarp();
@@ -548,7 +703,7 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams
 template <int BN, int EPI, int NP>
 int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t st) {
   static bool attr_set = false;
-  constexpr size_t smem = smem2_bytes<BN>();
+  constexpr size_t smem = smem2_bytes<BN, EPI>();
   if (!attr_set) {
     VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
@@ -635,9 +790,55 @@ int gemm_tc_pick_bn(int N, int np) {
   return best;
 }
 
+// The north-star extension epilogues (EPI_QKVN / EPI_GELU / EPI_F32G) run on
+// the CTA-pair kernel only (one pair per cluster, any M: rows past M are TMA
+// zero fill).  EPI_QKVN needs head-aligned tiles: BN a multiple of the padded
+// head dim and the launch's first column on a head boundary (the caller
+// starts each launch at a segment base).
+static int launch_gemm_tc_ext(const void* A, int64_t lda, const void* B, int64_t ldb,
+                              const GemmTcParams& p, int epi, cudaStream_t st) {
+  const int dp = epi == EPI_QKVN ? p.qkv.pad.DP : 16;
+  int bn = 0;
+  int64_t best = INT64_MAX;
+  for (int c : {256, 240, 160, 128}) {
+    if (c % dp) continue;
+    const int64_t pad = cdiv(p.N, c) * c - p.N;
+    if (pad < best) { best = pad; bn = c; }
+  }
+  if (!bn) { set_error("no head-aligned GEMM tile for padded head dim %d", dp); return VC_ENOTSUP; }
+  CUtensorMap ta, tb;
+  VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
+  VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn / 2, CU_TENSOR_MAP_SWIZZLE_128B));
+  if (epi == EPI_QKVN) {
+    if (dp == 64 && bn == 256) return launch_impl2<256, EPI_QKVN | (64 << 8), 1>(ta, tb, p, st);
+    if (dp == 64 && bn == 128) return launch_impl2<128, EPI_QKVN | (64 << 8), 1>(ta, tb, p, st);
+    if (dp == 80 && bn == 240) return launch_impl2<240, EPI_QKVN | (80 << 8), 1>(ta, tb, p, st);
+    if (dp == 80 && bn == 160) return launch_impl2<160, EPI_QKVN | (80 << 8), 1>(ta, tb, p, st);
+    if (dp == 128 && bn == 256) return launch_impl2<256, EPI_QKVN | (128 << 8), 1>(ta, tb, p, st);
+    if (dp == 128 && bn == 128) return launch_impl2<128, EPI_QKVN | (128 << 8), 1>(ta, tb, p, st);
+  }
+#define VC_GEMM_EXT(BNV)                                                             \
+  if (bn == BNV) return epi == EPI_GELU ? launch_impl2<BNV, EPI_GELU, 1>(ta, tb, p, st) \
+                                        : launch_impl2<BNV, EPI_F32G, 1>(ta, tb, p, st);
+  VC_GEMM_EXT(256)
+  VC_GEMM_EXT(240)
+  VC_GEMM_EXT(160)
+  VC_GEMM_EXT(128)
+#undef VC_GEMM_EXT
+  set_error("internal: no extension GEMM for epilogue %d tile %d", epi, bn);
+  return VC_ENOTSUP;
+}
+
 int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const GemmTcParams& p,
                    int epi, cudaStream_t st, int bn) {
   if (p.M <= 0 || p.N <= 0) return VC_OK;
+  if (epi >= EPI_QKVN) {
+    if (p.K <= 0 || (lda * 2) % 16 || (ldb * 2) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) {
+      set_error("tcgen05 GEMM needs 16-byte aligned operands and row pitches");
+      return VC_EINVAL;
+    }
+    return launch_gemm_tc_ext(A, lda, B, ldb, p, epi, st);
+  }
   if (p.K <= 0 || (lda * 2) % 16 || (ldb * 2) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) {
     set_error("tcgen05 GEMM needs 16-byte aligned operands and row pitches (lda %lld ldb %lld)",
               (long long)lda, (long long)ldb);

@@ -7,7 +7,13 @@
 
 namespace vc {
 
-enum { EPI_F32 = 0, EPI_BF16 = 1, EPI_QKV = 2 };
+enum {
+  EPI_F32 = 0, EPI_BF16 = 1, EPI_QKV = 2,
+  // north-star extensions (vc_ext.cu; parity unpinned, see oracle/vchitect_ext_oracle.py)
+  EPI_QKVN = 3,  // EPI_QKV + per-head QK-RMSNorm and 3D RoPE on the spatial / full-seq Q, K
+  EPI_GELU = 4,  // out bf16 = gelu_tanh(acc + bias[n])                  (FFN up-projection)
+  EPI_F32G = 5,  // out fp32 = R[m][n] + gate[n] * (acc + bias[n])        (gated residual)
+};
 
 // Attention-layout destination of one branch (spatial or full-sequence).
 struct BranchOut {
@@ -34,6 +40,16 @@ struct QkvScatter {
   int32_t Hg;
   int64_t send_rows;  // local rows M_r
   __nv_bfloat16* send;
+  // EPI_QKVN: RMSNorm weights [dh] per branch (0 spatial, 1 full sequence),
+  // RoPE (cos, sin) tables: rope[pos_t * nt + j] (frames), then
+  // rope[rope_off_y + y * ny + j] and rope[rope_off_x + x * nx + j] (patch
+  // grid rows / columns, gw columns); pair i < nt is temporal, i < nt + ny row,
+  // else column.  Text rows carry no position (no rotation).
+  const float* qn[2];
+  const float* kn[2];
+  const float2* rope;
+  int32_t dh, rope_nt, rope_ny, rope_nx, gw;
+  int64_t rope_off_y, rope_off_x;
 };
 
 struct GemmTcParams {
@@ -43,6 +59,7 @@ struct GemmTcParams {
   float* out_f32; const float* R; int64_t ldr;
   __nv_bfloat16* out_bf16;
   int64_t ldo;
+  const float* gate;  // EPI_F32G: [N]
   QkvScatter qkv;
 };
 

@@ -31,6 +31,10 @@ template <typename OutT>
 int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
                    cudaStream_t st);
 
+// AdaLN-modulated LayerNorm rows (north-star extension): LN(x)*(1+scale)+shift
+int launch_ln_rows_mod(const float* x, int64_t n_x, const float* p, int64_t n_p, int D,
+                       const float* shift, const float* scale, __nv_bfloat16* out, cudaStream_t st);
+
 int launch_embed(const float* lat, const float* w_in, float* x, int F, int first_frame, int tok0,
                  int ntok, int h, int w, int c, int p, int D, double t, cudaStream_t st);
 // Optional DDPM reverse step fused into the unembed (diffusion.py:95-116):
@@ -81,8 +85,29 @@ void profile_end();
 // bf16 tensor-core path (vc_block_bf16.cu)
 size_t bf16_workspace_bytes(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H);
 int bf16_launch_count(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H);
+// North-star extensions of the bf16 block (vc_ext.cu; parity unpinned,
+// oracle/vchitect_ext_oracle.py): AdaLN modulation, QK-RMSNorm + 3D RoPE in
+// the QKV epilogue, gated residual, gated GELU FFN.
+struct ExtArgs {
+  const float* mod;     // [6][D] shift_msa, scale_msa, gate_msa, shift_mlp, scale_mlp, gate_mlp
+  const float* qn[2];   // RMSNorm weights [dh]: spatial, full sequence
+  const float* kn[2];
+  const float2* rope;   // (cos, sin) tables, layout in QkvScatter
+  int32_t rope_nt, rope_ny, rope_nx, gw;
+  int64_t rope_off_y, rope_off_x;
+  int64_t Dff;
+  const void* w1;       // bf16 [Dff][D] (K-major B operand)
+  const float* b1;      // [Dff]
+  const void* w2;       // bf16 [D][Dff]
+  const float* b2;      // [D]
+  __nv_bfloat16* u;     // FFN hidden [Nv][Dff] (workspace)
+};
 int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, const void* wqkv,
                        const float* bias, const void* wo, const float* x, const float* prompt,
-                       float* out, int add_residual, char* ws, cudaStream_t st);
+                       float* out, int add_residual, char* ws, cudaStream_t st,
+                       const ExtArgs* ext = nullptr);
+// bytes of the bf16 block workspace region holding the O-GEMM A operand
+// (acat, [Nv][3D] bf16), reused by the extension as the FFN hidden when Dff <= 3D
+size_t bf16_workspace_acat_offset(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H);
 
 }  // namespace vc

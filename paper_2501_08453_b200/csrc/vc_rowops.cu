@@ -12,10 +12,14 @@ namespace vc {
 // the visual tokens then the (anchored, deduplicated) prompt rows.
 // One warp per row; the row is held in registers between the passes.
 // ---------------------------------------------------------------------------
-template <typename OutT, int VPL>
+// MOD (north-star AdaLN extension, oracle/vchitect_ext_oracle.py): the
+// normalised row is modulated, LN(x) * (1 + scale) + shift, before the store.
+template <typename OutT, int VPL, bool MOD = false>
 __global__ void __launch_bounds__(256) ln_rows_kernel(const float* __restrict__ x, int64_t n_x,
                                                       const float* __restrict__ p, int64_t n_p,
-                                                      int D, OutT* __restrict__ out) {
+                                                      int D, OutT* __restrict__ out,
+                                                      const float* __restrict__ shift = nullptr,
+                                                      const float* __restrict__ scale = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n_x + n_p) return;
@@ -41,7 +45,11 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const float* __restrict__ 
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     int d = lane + 32 * i;
-    if (d < D) dst[d] = from_f32<OutT>((v[i] - mean) * rstd);
+    if (d < D) {
+      float y = (v[i] - mean) * rstd;
+      if constexpr (MOD) y = fmaf(y, 1.f + __ldg(scale + d), __ldg(shift + d));
+      dst[d] = from_f32<OutT>(y);
+    }
   }
 }
 
@@ -65,6 +73,25 @@ int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int
 }
 template int launch_ln_rows<float>(const float*, int64_t, const float*, int64_t, int, float*, cudaStream_t);
 template int launch_ln_rows<__nv_bfloat16>(const float*, int64_t, const float*, int64_t, int, __nv_bfloat16*, cudaStream_t);
+
+int launch_ln_rows_mod(const float* x, int64_t n_x, const float* p, int64_t n_p, int D,
+                       const float* shift, const float* scale, __nv_bfloat16* out, cudaStream_t st) {
+  int64_t rows = n_x + n_p;
+  if (rows <= 0) return VC_OK;
+  dim3 grid((unsigned)cdiv(rows, 8));
+  int vpl = (int)cdiv(D, 32);
+  typedef __nv_bfloat16 bf;
+  if (vpl <= 4) ln_rows_kernel<bf, 4, true><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out, shift, scale);
+  else if (vpl <= 16) ln_rows_kernel<bf, 16, true><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out, shift, scale);
+  else if (vpl <= 50) ln_rows_kernel<bf, 50, true><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out, shift, scale);
+  else if (vpl <= 96) ln_rows_kernel<bf, 96, true><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out, shift, scale);
+  else {
+    set_error("LayerNorm supports dim <= 3072, got %d", D);
+    return VC_ENOTSUP;
+  }
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
 
 // ---------------------------------------------------------------------------
 // Patch embed, model.py:303-314 with patchify model.py:53-64 and
