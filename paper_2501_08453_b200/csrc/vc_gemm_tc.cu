@@ -45,21 +45,26 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 // ---- QKV scatter (EPI_QKV) ----
 // GEMM row m -> Q row / K row / (sequence, key) of the attention layouts.
-__device__ __forceinline__ void qkv_rows(const QkvScatter& s, int b, int64_t m, int64_t& qrow,
+__device__ __forceinline__ int qkv_frame(const QkvScatter& s, int64_t m) { return (int)m / (int)s.Lv; }
+// sp_f: frame of row m (qkv_frame), hoisted out of the chunk loop by the caller
+__device__ __forceinline__ void qkv_rows(const QkvScatter& s, int b, int64_t m, int sp_f, int64_t& qrow,
                                          int64_t& krow, int64_t& seq, int64_t& key) {
+  // 32-bit index math (rows < 2^31): a 64-bit division is a long software
+  // sequence and the epilogue runs it per chunk
+  const int mi = (int)m, Lv = (int)s.Lv, Lt = (int)s.Lt;
   if (s.text_rows) {            // prompt rows: full-sequence keys [0, Lt), no queries
-    qrow = -1; krow = m; seq = 0; key = m;
+    qrow = -1; krow = mi; seq = 0; key = mi;
   } else if (b == 0) {          // spatial: one sequence per frame
-    qrow = m; krow = m; seq = m / s.Lv; key = m - seq * s.Lv;
+    qrow = mi; krow = mi; seq = sp_f; key = mi - sp_f * Lv;
   } else {                      // full sequence: text keys first, then visual
-    qrow = m; krow = m + s.Lt; seq = 0; key = m + s.Lt;
+    qrow = mi; krow = mi + Lt; seq = 0; key = mi + Lt;
   }
 }
 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m, int n0,
                                                const uint32_t (&r)[16], const float* sbias,
-                                               const float* sgate = nullptr) {
+                                               const float* sgate = nullptr, int sp_f = -1) {
   if (m >= p.M) return;
   float v[16];
 #pragma unroll
@@ -159,10 +164,11 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
       return;
     }
     const int b = n < 3 * q.SEG ? 0 : 2;
-    const int64_t r = b == 0 ? n : n - q.fs_base();
-    const int which = (int)(r / q.SEG);
-    const int64_t jj = r - which * q.SEG;
-    const int hg = (int)(jj / q.DP), d0 = (int)(jj % q.DP);  // 16 | DP: the chunk is inside head hg
+    const int r = (int)(b == 0 ? n : n - q.fs_base());  // 32-bit: column indices are small
+    const int seg = (int)q.SEG;
+    const int which = r / seg;
+    const int jj = r - which * seg;
+    const int hg = jj / q.DP, d0 = jj - hg * q.DP;  // 16 | DP: the chunk is inside head hg
     if (s.mode == 1) {  // sequence-parallel send layout, branch-major: [b'][g][which][m][Hg][DP]
       const int g = hg / s.Hg, hl = hg - g * s.Hg;
       const int P = s.H / s.Hg;
@@ -181,7 +187,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
     const int h = hg - s.head_base;
     const BranchOut& bo = b == 0 ? s.sp : s.fs;
     int64_t qrow, krow, seq, key;
-    qkv_rows(s, b, m, qrow, krow, seq, key);
+    qkv_rows(s, b, m, sp_f >= 0 ? sp_f : qkv_frame(s, m), qrow, krow, seq, key);
     if (which < 2) {
       const int64_t row = which == 0 ? qrow : krow;
       if (row < 0) return;
@@ -195,8 +201,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
       reinterpret_cast<uint4*>(o)[1] = c;
     } else {  // V^T: 16 head dims of one key; lanes are consecutive keys (coalesced)
       __nv_bfloat16* o = bo.vt + ((seq * s.H + h) * q.DP + d0) * bo.ld_key + key;
+      const int64_t ld = bo.ld_key;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[(int64_t)i * bo.ld_key] = __float2bfloat16_rn(v[i]);
+      for (int i = 0; i < 16; ++i, o += ld) *o = __float2bfloat16_rn(v[i]);
     }
   }
 }
@@ -242,19 +249,27 @@ __device__ __forceinline__ void qkvn_head(const GemmTcParams& p, int64_t m, int 
   float v[DP];
   float ss4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 partial sums: short dependency chains
 #pragma unroll
-  for (int d = 0; d < DP; ++d) {
-    v[d] = __uint_as_float(u[d]) + (sbias ? sbias[d] : 0.f);
-    ss4[d & 3] = fmaf(v[d], v[d], ss4[d & 3]);  // padding columns are exact zeros (zero weights and bias)
+  for (int d = 0; d < DP; d += 4) {
+    // bias: one 16-byte smem broadcast per 4 columns (the head block is 16-byte aligned)
+    const float4 bb = sbias ? *reinterpret_cast<const float4*>(sbias + d) : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[d] = __uint_as_float(u[d]) + bb.x; v[d + 1] = __uint_as_float(u[d + 1]) + bb.y;
+    v[d + 2] = __uint_as_float(u[d + 2]) + bb.z; v[d + 3] = __uint_as_float(u[d + 3]) + bb.w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ss4[j] = fmaf(v[d + j], v[d + j], ss4[j]);  // padding columns are exact zeros
   }
   const float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
   const int bi = b == 0 ? 0 : 1;
-  const float* w = which == 0 ? s.qn[bi] : s.kn[bi];
+  const float2* w2 = reinterpret_cast<const float2*>(which == 0 ? s.qn[bi] : s.kn[bi]);  // dh even: 8-byte aligned
   const float rs = rsqrtf(ss / (float)s.dh + 1e-6f);
 #pragma unroll
-  for (int d = 0; d < DP; ++d)
-    if (d < s.dh) v[d] *= rs * __ldg(w + d);
+  for (int i = 0; i < DP / 2; ++i)
+    if (2 * i < s.dh) {
+      const float2 w = __ldg(w2 + i);
+      v[2 * i] *= rs * w.x;
+      v[2 * i + 1] *= rs * w.y;
+    }
   int64_t qrow, krow, seq, key;
-  qkv_rows(s, b, m, qrow, krow, seq, key);
+  qkv_rows(s, b, m, qkv_frame(s, m), qrow, krow, seq, key);
   if (!s.text_rows) {  // visual token: (frame, row, column) rotation
     const int64_t f = m / s.Lv, l = m - f * s.Lv;
     const int y = (int)(l / s.gw), x = (int)(l - (int64_t)(l / s.gw) * s.gw);
@@ -451,9 +466,9 @@ template <int BN>
 constexpr int stages2_for() {
   return (216 * 1024) / (BM * BK * 2 + (BN / 2) * BK * 2) > 8 ? 8 : (216 * 1024) / (BM * BK * 2 + (BN / 2) * BK * 2);
 }
-template <int BN, int EPI>
-constexpr size_t smem2_bytes() {  // stages + barriers + bias staging (+ gate staging, EPI_F32G) + align
-  return (size_t)stages2_for<BN>() * (BM * BK * 2 + (BN / 2) * BK * 2) + 256 + 4 * 256 * 4 +
+template <int BN, int EPI, int EW = 4>
+constexpr size_t smem2_bytes() {  // stages + barriers + bias staging per epilogue warp (+ gate, EPI_F32G) + align
+  return (size_t)stages2_for<BN>() * (BM * BK * 2 + (BN / 2) * BK * 2) + 256 + EW * 256 * 4 +
          (EPI == EPI_F32G ? 4 * 256 * 4 : 0) + 1024;
 }
 
@@ -462,8 +477,14 @@ constexpr size_t smem2_bytes() {  // stages + barriers + bias staging (+ gate st
 // loads 64-row slice p of each CTA's 128-row A half and multicasts it to the
 // same-rank CTA of the other pair, halving the A bytes each SM pulls from L2
 // (the pair kernel was L2 -> SMEM bound: 9.3 GB of L2 reads for the QKV GEMM).
-template <int BN, int EPI, int NP>
-__global__ void __launch_bounds__(kThreads, 1)
+//
+// EW = epilogue warps (4 or 8).  The QKV scatter epilogue (V^T transposed
+// stores, per-chunk layout math) is slower than the 25 k-block main loop of
+// a K = D tile: with 4 warps the MMA warp waits on tempty (ncu: the QKV GEMM
+// was epilogue-bound).  EW = 8 puts two warps on each TMEM lane quarter
+// (warp w reads lanes 32 * (w % 4)), splitting the tile's 16-column chunks.
+template <int BN, int EPI, int NP, int EW = 4>
+__global__ void __launch_bounds__(128 + 32 * EW, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -502,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (NP = 2: the A slice this CTA loads also lands in the other pair)
     for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], NP); }
     // tempty (leader): one arrival per epilogue warp of both CTAs
-    for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * 4); }
+    for (int a = 0; a < 2; ++a) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * EW); }
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, 512);
@@ -563,10 +584,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
+    const int q = warp & 3;           // TMEM lane quarter
+    const int ew = warp - 4;          // epilogue warp index
+    const int sub = ew >> 2;          // which of the EW / 4 warps on this quarter
     const int lane = threadIdx.x & 31;
-    float* sbias = sbias_all + q * 256;
-    float* sgate = sbias_all + 4 * 256 + q * 256;  // EPI_F32G only (smem2_bytes)
+    float* sbias = sbias_all + ew * 256;
+    float* sgate = sbias_all + EW * 256 + q * 256;  // EPI_F32G only (smem2_bytes)
     const uint32_t tempty_leader = ptx::mapa_shared(ptx::smem_u32(tempty), (uint32_t)(2 * pair));
     int local = 0;
     for (int t = cluster; t < tiles; t += nclusters, ++local) {
@@ -614,14 +637,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           qkvn_head<EDP>(p, m, n0, tbase + hb * EDP, p.bias ? sbias + hb * EDP : nullptr);
         }
       } else {
+        const int sp_f = EPI == EPI_QKV && m < p.M ? qkv_frame(p.qkv, m) : 0;
 #pragma unroll 1
-        for (int c = 0; c < BN / 16; ++c) {
+        for (int c = sub; c < BN / 16; c += EW / 4) {
           const int n0 = nt * BN + c * 16;
           if (n0 >= p.N || mrow0 >= p.M) break;
           uint32_t r[16];
           ptx::tmem_ld16(tbase + c * 16, r);
           ptx::tmem_ld_wait();
-          epilogue_chunk<EPI>(p, m, n0, r, p.bias ? sbias + c * 16 : nullptr, sgate + c * 16);
+          epilogue_chunk<EPI>(p, m, n0, r, p.bias ? sbias + c * 16 : nullptr, sgate + c * 16, sp_f);
         }
       }
       ptx::fence_before_sync();
@@ -700,18 +724,18 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams
   return VC_OK;
 }
 
-template <int BN, int EPI, int NP>
+template <int BN, int EPI, int NP, int EW = 4>
 int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams& p, cudaStream_t st) {
   static bool attr_set = false;
-  constexpr size_t smem = smem2_bytes<BN, EPI>();
+  constexpr size_t smem = smem2_bytes<BN, EPI, EW>();
   if (!attr_set) {
-    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    VC_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<BN, EPI, NP, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     attr_set = true;
   }
   const int64_t ctiles = cdiv(p.M, 2 * BM) * cdiv(cdiv(p.N, BN), NP);
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(128 + 32 * EW);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -724,14 +748,14 @@ int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParam
   static int resident = 0;  // co-resident clusters (see launch_impl)
   if (!resident) {
     cfg.gridDim = dim3((unsigned)(num_sms() / (2 * NP) * 2 * NP));
-    if (cudaOccupancyMaxActiveClusters(&resident, gemm_tc2_kernel<BN, EPI, NP>, &cfg) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveClusters(&resident, gemm_tc2_kernel<BN, EPI, NP, EW>, &cfg) != cudaSuccess ||
         resident <= 0)
       resident = num_sms() / (2 * NP);
     if (getenv("VC_GEMM_DEBUG")) fprintf(stderr, "gemm_tc2 NP=%d: %d resident clusters\n", NP, resident);
   }
   const int clusters = (int)std::min<int64_t>(ctiles, resident);
   cfg.gridDim = dim3((unsigned)(clusters * 2 * NP));
-  VC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI, NP>, ta, tb, p));
+  VC_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI, NP, EW>, ta, tb, p));
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
@@ -851,6 +875,8 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
   // overrides.  (Before the grid was sized with cudaOccupancyMaxActiveClusters
   // the 4-CTA clusters ran in two waves and looked 1.7x slower.)
   static const int np_env = getenv("VC_GEMM_NP") ? atoi(getenv("VC_GEMM_NP")) : 0;
+  // epilogue warps of the QKV scatter (8 default; VC_GEMM_EW=4 is the A/B switch)
+  static const int ew = getenv("VC_GEMM_EW") ? atoi(getenv("VC_GEMM_EW")) : 8;
   // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
   // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
   static const bool no_mc = getenv("VC_GEMM_NO_MC") != nullptr;
@@ -872,7 +898,8 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
     if (pair && np == 2) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32, 2>(ta, tb, p, st)  \
                                                : launch_impl2<BNV, EPI_QKV, 2>(ta, tb, p, st); \
     if (pair) return epi == EPI_F32 ? launch_impl2<BNV, EPI_F32, 1>(ta, tb, p, st)           \
-                                    : launch_impl2<BNV, EPI_QKV, 1>(ta, tb, p, st);          \
+                                    : (ew == 8 ? launch_impl2<BNV, EPI_QKV, 1, 8>(ta, tb, p, st) \
+                                               : launch_impl2<BNV, EPI_QKV, 1>(ta, tb, p, st)); \
     if (epi == EPI_BF16) return launch_impl<BNV, EPI_BF16, 1>(ta, tb, p, st);                \
     if (cm == 4 && (BNV / 4) % 8 == 0)                                                       \
       return epi == EPI_F32 ? launch_impl<BNV, EPI_F32, ((BNV / 4) % 8 == 0 ? 4 : 2)>(ta, tb, p, st) \
