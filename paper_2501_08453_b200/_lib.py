@@ -92,11 +92,13 @@ def load():
     """Load the library (no GPU needed to load or to query sizes)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        # VC_LIB_PATH: A/B aid for profiling two builds on one box (tools/)
+        path = os.environ.get("VC_LIB_PATH", LIB_PATH)
+        if not os.path.exists(path):
             raise RuntimeError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_2501_08453_b200.build` "
+                f"{path} is missing: build it with `python -m paper_2501_08453_b200.build` "
                 "(the CUDA path has no fallback)")
-        lib = C.CDLL(LIB_PATH)
+        lib = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

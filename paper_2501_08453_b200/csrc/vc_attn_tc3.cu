@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
   // the last CTA of a sequence may have no rows in its second query tile
   // (e.g. 1350 = 5 x 256 + 70): then only tile A runs (CTA-uniform)
   const int ntile = q0 + BQ < p.Lq ? 2 : 1;
-  [[maybe_unused]] const bool tr = blockIdx.x == 20 && blockIdx.y == 3 && blockIdx.z == 0;
+  [[maybe_unused]] const bool tr = blockIdx.x == min(20u, gridDim.x - 1) && blockIdx.y == 3 && blockIdx.z == 0;
+  VC_TR3(tr && threadIdx.x == 32, 0, 255, 0);  // entry (trace builds: CTA fixed-cost marks in j = 255)
 
   if (warp == 0 && ptx::elect_one()) {
     ptx::prefetch_tmap(&tmQ64); ptx::prefetch_tmap(&tmK64); ptx::prefetch_tmap(&tmV);
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
   __syncthreads();
   ptx::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  VC_TR3(tr && threadIdx.x == 32, 0, 255, 1);  // barriers + TMEM ready
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -204,7 +206,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
       __syncwarp();
     };
     const bool trm = tr && (threadIdx.x & 31) == 0;
+    VC_TR3(trm, 0, 255, 2);  // Q landed
     ptx::mbar_wait(&k_full[0], 0);
+    VC_TR3(trm, 0, 255, 3);  // first K block landed
     issue_s(0, 0);
     if (ntile == 2) issue_s(1, 0);
     for (int j = 0; j < n_tiles; ++j) {
@@ -376,6 +380,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       }
       ptx::mbar_wait(&pv_done[t], (n_tiles - 1) & 1);
       ptx::fence_after_sync();
+      VC_TR3(trs, 1 + sw, 255, 0);  // last P.V done
       if (ONES) {  // row sum accumulated by the tensor core in the ones column
         uint32_t r1;
         ptx::tmem_ld1(tO + p.dh, r1);
@@ -394,10 +399,12 @@ __global__ void __launch_bounds__(kThreads3, 1)
       }
       if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
       else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
+      VC_TR3(trs, 1 + sw, 255, 1);  // output stored
     }
   }
   ptx::fence_before_sync();
   __syncthreads();
+  VC_TR3(tr && threadIdx.x == 32, 0, 255, 4);  // all warps done
   if (warp == 1) {
     ptx::fence_after_sync();
     ptx::tmem_dealloc(tmem, 512);

@@ -117,25 +117,24 @@ __device__ __forceinline__ void store_p(uint32_t p_tile, int row, const float (&
 // O / l -> bf16 -> output row of query qi of sequence seq, head h (plain
 // [row][ld_out] at col_off, or the sequence-parallel a2a #2 send layout).
 // C0..C1: the 16-column chunks of O this thread writes (all by default).
+// Output row of query qi (sequence seq, head h): plain [seq * out_seq_rows + qi]
+// rows, or the sequence-parallel branch-major send blocks (spo).
+__device__ __forceinline__ __nv_bfloat16* out_row(const AttnTcParams& p, int qi, int seq, int h) {
+  if (p.spo.P == 0) return p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off + (int64_t)h * p.dh;
+  const int f = p.spo.branch == 0 ? seq : qi / p.spo.Lv;
+  const int lpos = p.spo.branch == 0 ? qi : qi - f * p.spo.Lv;
+  int r = 0;
+  while (r + 1 < p.spo.P && p.spo.vb[r + 1] <= lpos) ++r;
+  const int vc = p.spo.vb[r + 1] - p.spo.vb[r];
+  // base[r] already points at this branch's block for rank r
+  return p.out + p.spo.base[r] + ((int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg + (int64_t)h * p.dh;
+}
+
 template <int DP, int C0 = 0, int C1 = DP / 16>
 __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr, float l, int qi, int seq,
                                           int h) {
   const float inv = 1.f / l;
-  __nv_bfloat16* orow = nullptr;
-  if (qi < p.Lq) {
-    if (p.spo.P == 0) {
-      orow = p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off + (int64_t)h * p.dh;
-    } else {
-      const int f = p.spo.branch == 0 ? seq : qi / p.spo.Lv;
-      const int lpos = p.spo.branch == 0 ? qi : qi - f * p.spo.Lv;
-      int r = 0;
-      while (r + 1 < p.spo.P && p.spo.vb[r + 1] <= lpos) ++r;
-      const int vc = p.spo.vb[r + 1] - p.spo.vb[r];
-      const int64_t Mr = (int64_t)p.spo.F * vc;
-      (void)Mr;  // base[r] already points at this branch's block for rank r
-      orow = p.out + p.spo.base[r] + ((int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg + (int64_t)h * p.dh;
-    }
-  }
+  __nv_bfloat16* orow = qi < p.Lq ? out_row(p, qi, seq, h) : nullptr;
 #pragma unroll
   for (int c = C0; c < C1; ++c) {
     uint32_t r[16];
