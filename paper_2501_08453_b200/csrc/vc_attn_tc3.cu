@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         ptx::tma_load_4d(sV, &tmV, &v_full[s], k0, 0, h, seq);
         ptx::tma_load_4d(sV + DP * 128, &tmV, &v_full[s], k0 + 64, 0, h, seq);
       }
+      VC_TR3(tr, 0, 254, 0);  // TMA producer issued its last load
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         VC_TR3(trm, 0, j, 5);
       }
     }
+    VC_TR3(trm, 0, 254, 1);  // MMA issuer done
   } else {
     // ===================== softmax (tile t, key half), correction, epilogue =====================
     const int sw = warp - 2;
@@ -397,8 +399,20 @@ __global__ void __launch_bounds__(kThreads3, 1)
         ptx::tmem_ld_wait();
         l += __uint_as_float(other);
       }
+      VC_TR3(trs, 1 + sw, 255, 2);  // row sum read
+#ifdef VC_ATTN_STAGED_OUT
+      {  // rows staged in this tile's K stage (free once the tile's last P.V is done), copied out a warp per row
+        const int sdh = (p.dh + 1) & ~1;
+        __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + CF::OFF_K + t * CF::QK_BYTES);
+        if (half == 0) stage_out<DP, 0, CF::NC0>(tO, l, stg + row * sdh, p.dh);
+        else stage_out<DP, CF::NC0, CF::NC>(tO, l, stg + row * sdh, p.dh);
+        ptx::named_bar_sync(9 + t, 256);
+        copy_out_rows(p, stg, sdh, q0 + t * BQ, BQ, seq, h, sw & 7, 8, lane);
+      }
+#else
       if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
       else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
+#endif
       VC_TR3(trs, 1 + sw, 255, 1);  // output stored
     }
   }

@@ -38,14 +38,14 @@ int main(int argc, char** argv) {
   __nv_bfloat16 *q, *k, *vt, *out;
   const size_t nq = (size_t)Lq * H * DP, nk = (size_t)Lk * H * DP, nv = (size_t)H * DP * ld_key;
   cudaMalloc(&q, nq * 2); cudaMalloc(&k, nk * 2); cudaMalloc(&vt, nv * 2);
-  cudaMalloc(&out, (size_t)Lq * H * dh * 2);
+  cudaMalloc(&out, (size_t)Lq * H * 80 * 2 + 4096);
   fill_kernel<<<1024, 256>>>(q, nq, 1, 2.f);
   fill_kernel<<<1024, 256>>>(k, nk, 2, 2.f);
   fill_kernel<<<1024, 256>>>(vt, nv, 3, 1.f);
   vc::AttnTcParams p{};
   p.Lq = Lq; p.Lk = Lk; p.H = H; p.dh = dh; p.n_bias = n_bias;
   p.bias_log2 = 2.f; p.scale_log2 = 1.4426950408889634f / sqrtf((float)dh);
-  p.out = out; p.ld_out = (int64_t)H * dh; p.col_off = 0; p.out_seq_rows = Lq;
+  p.out = getenv("VC_TRACE_NO_OUT") ? nullptr : out; p.ld_out = getenv("VC_TRACE_LD80") ? (int64_t)H * 80 : (int64_t)H * dh; p.col_off = 0; p.out_seq_rows = Lq;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   int rc = vc::launch_attn_tc(p, q, k, vt, 1, Lq, Lk, ld_key, DP, 0);
