@@ -53,11 +53,82 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const float* __restrict__ 
   }
 }
 
+// bf16 output, D % 4 == 0: 16-byte loads and 8-byte stores (the row kernel
+// above issues 4-byte loads; this one keeps 4x more bytes in flight per load).
+template <int NV, bool MOD>
+__global__ void __launch_bounds__(256) ln_rows_v4_kernel(const float* __restrict__ x, int64_t n_x,
+                                                         const float* __restrict__ p, int64_t n_p, int D,
+                                                         __nv_bfloat16* __restrict__ out,
+                                                         const float* __restrict__ shift,
+                                                         const float* __restrict__ scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n_x + n_p) return;
+  const float4* src = reinterpret_cast<const float4*>(row < n_x ? x + row * D : p + (row - n_x) * D);
+  const int D4 = D >> 2;
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < D4 ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mean = warp_sum(s) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (lane + 32 * i < D4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+      q = fmaf(a, a, fmaf(b, b, fmaf(c, c, fmaf(d, d, q))));
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / D + 1e-5f);
+  uint2* dst = reinterpret_cast<uint2*>(out + row * D);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < D4) {
+      float y0 = (v[i].x - mean) * rstd, y1 = (v[i].y - mean) * rstd;
+      float y2 = (v[i].z - mean) * rstd, y3 = (v[i].w - mean) * rstd;
+      if constexpr (MOD) {
+        const float4 sc = __ldg(reinterpret_cast<const float4*>(scale) + c);
+        const float4 sh = __ldg(reinterpret_cast<const float4*>(shift) + c);
+        y0 = fmaf(y0, 1.f + sc.x, sh.x); y1 = fmaf(y1, 1.f + sc.y, sh.y);
+        y2 = fmaf(y2, 1.f + sc.z, sh.z); y3 = fmaf(y3, 1.f + sc.w, sh.w);
+      }
+      __nv_bfloat162 lo = __floats2bfloat162_rn(y0, y1), hi = __floats2bfloat162_rn(y2, y3);
+      dst[c] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  }
+}
+
+template <bool MOD>
+int launch_ln_rows_v4(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, __nv_bfloat16* out,
+                      const float* shift, const float* scale, cudaStream_t st) {
+  const int64_t rows = n_x + n_p;
+  if (rows <= 0) return VC_OK;
+  dim3 grid((unsigned)cdiv(rows, 8));
+  const int nv = (int)cdiv(D / 4, 32);
+  if (nv <= 4) ln_rows_v4_kernel<4, MOD><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out, shift, scale);
+  else if (nv <= 13) ln_rows_v4_kernel<13, MOD><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out, shift, scale);
+  else if (nv <= 24) ln_rows_v4_kernel<24, MOD><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out, shift, scale);
+  else {
+    set_error("LayerNorm supports dim <= 3072, got %d", D);
+    return VC_ENOTSUP;
+  }
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
 template <typename OutT>
 int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
                    cudaStream_t st) {
   int64_t rows = n_x + n_p;
   if (rows <= 0) return VC_OK;
+  if constexpr (sizeof(OutT) == 2) {
+    if (D % 4 == 0) return launch_ln_rows_v4<false>(x, n_x, p, n_p, D, out, nullptr, nullptr, st);
+  }
   dim3 grid((unsigned)cdiv(rows, 8));
   int vpl = (int)cdiv(D, 32);
   if (vpl <= 4) ln_rows_kernel<OutT, 4><<<grid, 256, 0, st>>>(x, n_x, p, n_p, D, out);
@@ -78,6 +149,7 @@ int launch_ln_rows_mod(const float* x, int64_t n_x, const float* p, int64_t n_p,
                        const float* shift, const float* scale, __nv_bfloat16* out, cudaStream_t st) {
   int64_t rows = n_x + n_p;
   if (rows <= 0) return VC_OK;
+  if (D % 4 == 0) return launch_ln_rows_v4<true>(x, n_x, p, n_p, D, out, shift, scale, st);
   dim3 grid((unsigned)cdiv(rows, 8));
   int vpl = (int)cdiv(D, 32);
   typedef __nv_bfloat16 bf;
