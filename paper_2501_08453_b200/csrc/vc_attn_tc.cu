@@ -406,6 +406,14 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
   // CTA pairs; persistent) are in git history at 20e1484 and 028589b;
   // profiles/r01/attn_study/README.md.
   static const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 3;
+  // persistent tc3 (VC_ATTN_PERSIST, A/B switch): 0 (default) never, 1 short
+  // key ranges (<= 4096 keys: the spatial branch), 2 always.  Correct on every
+  // test shape, but measured 0.401-0.405 vs 0.396-0.399 ms on the spatial
+  // branch (profiles/r01/attn_study/README.md), so off.
+  static const int persist = getenv("VC_ATTN_PERSIST") ? atoi(getenv("VC_ATTN_PERSIST")) : 0;
+  const bool use_p = impl == 3 && (persist == 2 || (persist == 1 && p.Lk <= 4096)) && p.spo.P == 0;
+  if (use_p && DP == 64) return launch_attn_tc3p<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+  if (use_p && DP == 80) return launch_attn_tc3p<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
   switch (DP) {
     case 64:
       if (impl == 1) return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
