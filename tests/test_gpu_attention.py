@@ -112,3 +112,26 @@ def test_bf16_attention_random_shapes(vc):
             got = vc.attention(q, k, v, H, dtype="bf16")
             ref = O.attention(q, k, v, H)
         assert rel_l2(got, ref) <= BF16_TOL, (case, sq, sk, dh, H, rel_l2(got, ref))
+
+
+def test_persistent_variant_matches_oracle(vc):
+    # the persistent tc3 kernel (VC_ATTN_PERSIST=2, an A/B switch read once per
+    # process) on ragged shapes incl. single-tile query blocks, in a subprocess
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_2501_08453_b200 as vc\n"
+        "from oracle import spsim_oracle as O\n"
+        "r = np.random.default_rng(3)\n"
+        "for sq, sk, dh, H in [(1350, 1350, 66, 4), (70, 300, 64, 2), (600, 129, 80, 3), (5, 1, 66, 1)]:\n"
+        "    q, k, v = (r.standard_normal((n, dh * H)) for n in (sq, sk, sk))\n"
+        "    got = vc.attention(q, k, v, H, dtype='bf16')\n"
+        "    ref = O.attention(q, k, v, H)\n"
+        "    e = np.linalg.norm(got - ref) / np.linalg.norm(ref)\n"
+        "    assert e <= 2e-2, (sq, sk, dh, H, e)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VC_ATTN_PERSIST="2", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
