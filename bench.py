@@ -104,17 +104,20 @@ class ClockSampler:
         except Exception:
             return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
-    def _poll_nvml(self):
+    def _sample_nvml(self):
         nv, h = self.nvml
         bits = {"sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
                 "hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                 "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                 "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown}
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.samples.append((float(sm), float(mx), {k for k, b in bits.items() if r & b}))
+
+    def _poll_nvml(self):
         while True:
-            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            self.samples.append((float(sm), float(mx), {k for k, b in bits.items() if r & b}))
+            self._sample_nvml()
             if self.stop.wait(self.period):
                 break
 
@@ -123,6 +126,12 @@ class ClockSampler:
             self.nvml = self._nvml_handle()
             self.thread = threading.Thread(target=self._poll_nvml, daemon=True)
             self.thread.start()
+            # the poller is running before the timed region starts: wait for its
+            # first sample, then drop it (it predates the region)
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 2.0:
+                time.sleep(0.0005)
+            self.samples.clear()
             return self
         except Exception:
             self.nvml = None
@@ -145,6 +154,8 @@ class ClockSampler:
         if self.nvml:
             self.stop.set()
             self.thread.join(timeout=5)
+            if not self.samples:  # a region shorter than one poll: sample at its end
+                self._sample_nvml()
         if self.proc:
             self.proc.terminate()
             try:
