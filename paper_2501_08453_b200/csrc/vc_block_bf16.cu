@@ -87,10 +87,9 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     GemmTcParams g{};
     g.M = Nv; g.N = (int)pad.fs_base(); g.K = (int)D; g.bias = bias;
     g.qkv = sc; g.qkv.n_base = 0; g.qkv.text_rows = 0;
-    static const int plain = getenv("VC_EXT_QKV_PLAIN") ? atoi(getenv("VC_EXT_QKV_PLAIN")) : 0;  // A/B
-    VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, plain ? EPI_QKV : EPI_QKVN, st, plain == 2 ? 240 : 0));
+    VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_QKVN, st));
     g.N = (int)(3 * pad.SEG); g.bias = bias + pad.fs_base(); g.qkv.n_base = pad.fs_base();
-    VC_TRY(launch_gemm_tc(xhat, D, (const bf*)wqkv + pad.fs_base() * D, D, g, plain ? EPI_QKV : EPI_QKVN, st, plain == 2 ? 240 : 0));
+    VC_TRY(launch_gemm_tc(xhat, D, (const bf*)wqkv + pad.fs_base() * D, D, g, EPI_QKVN, st));
   } else {
     GemmTcParams g{};
     g.M = Nv; g.N = (int)pad.Npad; g.K = (int)D; g.bias = bias;
