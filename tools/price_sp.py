@@ -1,0 +1,27 @@
+"""Priced strong scaling of the SP block from this round's measured stage
+times (paper_2501_08453_b200.pricing; a MODEL, not a measurement — the pool
+has one GPU per box).  Writes profiles/r01/sp_pricing.json."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2501_08453_b200 import pricing  # noqa: E402
+
+SHAPES = {2: (16, 1350, 256, 1584, 24, "profiles/r01/bench_config2.json"),
+          4: (160, 1350, 256, 1584, 24, "profiles/r01/configs/bench_cfg4.json"),
+          5: (64, 256, 256, 3072, 24, "profiles/r01/configs/bench_cfg5.json")}
+out = {"what": "PRICED (alpha-beta model on measured single-GPU stage times), not measured: "
+               "paper_2501_08453_b200/pricing.py; spec = B200Spec (NVLink 900 GB/s nominal, alpha 10 us assumed)",
+       "spec": pricing.B200Spec().as_cluster_kwargs(), "configs": {}}
+for cfg, (F, Lv, Lt, D, H, path) in SHAPES.items():
+    stages = json.load(open(os.path.join(ROOT, path)))["block"]["stage_ms"]
+    out["configs"][f"config{cfg}"] = {
+        "stage_ms_measured_1gpu": stages,
+        "overlapped": pricing.price_scaling(stages, F, Lv, Lt, D, H, ps=(1, 2, 3, 4, 6, 8)),
+        "exposed": pricing.price_scaling(stages, F, Lv, Lt, D, H, ps=(1, 2, 3, 4, 6, 8), overlap=False),
+    }
+json.dump(out, open(os.path.join(ROOT, "profiles/r01/sp_pricing.json"), "w"), indent=1)
+for k, v in out["configs"].items():
+    print(k, [(r["p"], round(r["ms"], 3), round(r["efficiency"], 3)) for r in v["overlapped"]])
