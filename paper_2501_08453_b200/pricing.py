@@ -67,9 +67,12 @@ _HEAD_STAGES = ("attn_spatial", "attn_fullseq", "text_kv_gemm")   # H/P heads (1
 
 
 def price_sp_block(stage_ms: dict, frames: int, visual_len: int, text_len: int, dim: int, heads: int,
-                   p: int, spec: B200Spec = B200Spec(), overlap: bool = True) -> dict:
+                   p: int, spec: B200Spec = B200Spec(), overlap: bool = True,
+                   sp_overhead_ms: float = 0.0) -> dict:
     """Priced time of one block forward on P ranks (slowest rank), from the
-    measured single-GPU stage times. Returns ms per block, the exchange bytes
+    measured single-GPU stage times. sp_overhead_ms: the SP path's extra
+    layout passes (exchange-buffer unpacks) measured at P = 1, divided over
+    the ranks like the activations. Returns ms per block, the exchange bytes
     per rank and the exposed communication."""
     if heads % p:
         raise ValueError(f"head-parallel pricing needs P | H ({p} does not divide {heads})")
@@ -98,20 +101,22 @@ def price_sp_block(stage_ms: dict, frames: int, visual_len: int, text_len: int, 
         hide_tm = compute.get("attn_temporal", 0.0)
         exposed = max(0.0, t1 - hide_tm) + max(0.0, t1 - compute.get("attn_spatial", 0.0)) \
             + max(0.0, t2 - compute.get("attn_fullseq", 0.0)) + t2
-    total = sum(compute.values()) + exposed
-    return {"p": p, "ms": total, "compute_ms": sum(compute.values()), "comm_ms": comm,
+    layout = sp_overhead_ms * row_share if p > 1 else 0.0
+    total = sum(compute.values()) + layout + exposed
+    return {"p": p, "ms": total, "compute_ms": sum(compute.values()) + layout, "comm_ms": comm,
             "exposed_comm_ms": exposed, "a2a1_bytes_per_branch": a2a1, "a2a2_bytes_per_branch": a2a2}
 
 
 def price_scaling(stage_ms: dict, frames: int, visual_len: int, text_len: int, dim: int, heads: int,
-                  ps=(1, 2, 4, 8), spec: B200Spec = B200Spec(), overlap: bool = True) -> list:
+                  ps=(1, 2, 4, 8), spec: B200Spec = B200Spec(), overlap: bool = True,
+                  sp_overhead_ms: float = 0.0) -> list:
     """Priced strong scaling: tokens/s and T1 / (P * TP) per P."""
     rows = []
     t1 = None
     for p in ps:
         if heads % p:
             continue
-        r = price_sp_block(stage_ms, frames, visual_len, text_len, dim, heads, p, spec, overlap)
+        r = price_sp_block(stage_ms, frames, visual_len, text_len, dim, heads, p, spec, overlap, sp_overhead_ms)
         t1 = r["ms"] if p == 1 else t1
         r["tokens_per_s"] = frames * visual_len / (r["ms"] / 1e3)
         r["efficiency"] = (t1 / (p * r["ms"])) if t1 else None

@@ -15,12 +15,19 @@ SHAPES = {2: (16, 1350, 256, 1584, 24, "profiles/r01/bench_config2.json"),
 out = {"what": "PRICED (alpha-beta model on measured single-GPU stage times), not measured: "
                "paper_2501_08453_b200/pricing.py; spec = B200Spec (NVLink 900 GB/s nominal, alpha 10 us assumed)",
        "spec": pricing.B200Spec().as_cluster_kwargs(), "configs": {}}
+# the SP path's layout passes, measured on config 2: SP at P = 1 (5.99 ms,
+# bench.py --sp under torchrun) minus the plain block (5.26 ms) minus the
+# world-1 NCCL all-to-all copy of 635 MB (~0.2 ms at HBM speed); scaled to the
+# other configs by activation size (memory-bound unpacks)
+SP_OVERHEAD_CFG2 = 5.99 - 5.26 - 0.20
 for cfg, (F, Lv, Lt, D, H, path) in SHAPES.items():
     stages = json.load(open(os.path.join(ROOT, path)))["block"]["stage_ms"]
+    ovh = SP_OVERHEAD_CFG2 * (F * Lv * D) / (16 * 1350 * 1584)
     out["configs"][f"config{cfg}"] = {
-        "stage_ms_measured_1gpu": stages,
-        "overlapped": pricing.price_scaling(stages, F, Lv, Lt, D, H, ps=(1, 2, 3, 4, 6, 8)),
-        "exposed": pricing.price_scaling(stages, F, Lv, Lt, D, H, ps=(1, 2, 3, 4, 6, 8), overlap=False),
+        "stage_ms_measured_1gpu": stages, "sp_layout_overhead_ms_at_p1": ovh,
+        "overlapped": pricing.price_scaling(stages, F, Lv, Lt, D, H, ps=(1, 2, 3, 4, 6, 8), sp_overhead_ms=ovh),
+        "exposed": pricing.price_scaling(stages, F, Lv, Lt, D, H, ps=(1, 2, 3, 4, 6, 8), overlap=False,
+                                         sp_overhead_ms=ovh),
     }
 json.dump(out, open(os.path.join(ROOT, "profiles/r01/sp_pricing.json"), "w"), indent=1)
 for k, v in out["configs"].items():
