@@ -145,9 +145,25 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
     const int64_t gpb = (Mr + 31) / 32;  // row groups per which-block
     const int64_t wl = w - a.groups[r];
     const int which = (int)(wl / gpb);
+    const int bp = a.branch, blk = which;
+    if (which < 2) {  // Q / K rows: the warp copies one row at a time, lanes across it (coalesced)
+      const int64_t m0 = (wl - which * gpb) * 32;
+      for (int rr = 0; rr < 32; ++rr) {
+        const int64_t m = m0 + rr;
+        if (m >= Mr) break;
+        const int f = (int)(m / vc), l = a.vb[r] + (int)(m - (int64_t)f * vc);
+        const int64_t tok = (int64_t)f * a.Lv + l;
+        const uint4* s4 = reinterpret_cast<const uint4*>(a.recv + a.off[r] + ((int64_t)blk * Mr + m) * rowlen);
+        __nv_bfloat16* dst;
+        if (bp == 0) dst = (which == 0 ? a.qsp : a.ksp) + tok * rowlen;
+        else dst = which == 0 ? a.qfs + tok * rowlen : a.kfs + (a.Lt + tok) * rowlen;
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (int i = lane; i < rowlen / 8; i += 32) d4[i] = s4[i];
+      }
+      continue;
+    }
     const int64_t m = (wl - which * gpb) * 32 + lane;
     if (m >= Mr) continue;
-    const int bp = a.branch, blk = which;
     const int f = (int)(m / vc), l = a.vb[r] + (int)(m - (int64_t)f * vc);
     const __nv_bfloat16* src = a.recv + a.off[r] + ((int64_t)blk * Mr + m) * rowlen;
     const int64_t tok = (int64_t)f * a.Lv + l;  // visual token index
@@ -174,19 +190,28 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
 }
 
 // recv2[b'][g][m][Dg] -> acat[m][b'*2D + g*Dg + c]  (b'=0 spatial cols [0,D), b'=1 full-seq [2D,3D))
-__global__ void sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv, __nv_bfloat16* __restrict__ acat,
-                                  int P, int64_t Mr, int64_t Dg, int64_t D) {
-  const int64_t words = Dg / 2;  // Dg even (dh even)
-  const int64_t total = (int64_t)P * 2 * Mr * words;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t wi = e % words;
-    const int64_t row = e / words;  // (b'*P + g)*Mr + m
+// One warp per (b', g, m) row, lanes across the row: 16-byte words when Dg and
+// D are multiples of 8 (every row then starts 16-byte aligned), else 4-byte.
+__global__ void __launch_bounds__(256) sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv,
+                                                         __nv_bfloat16* __restrict__ acat, int P, int64_t Mr,
+                                                         int64_t Dg, int64_t D) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)P * 2 * Mr;
+  const bool v16 = (Dg % 8) == 0 && (D % 8) == 0;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t m = row % Mr;
-    const int64_t gb = row / Mr;
+    const int64_t gb = row / Mr;  // b'*P + g
     const int bp = (int)(gb / P), g = (int)(gb % P);
-    const uint32_t v = reinterpret_cast<const uint32_t*>(recv + row * Dg)[wi];
-    reinterpret_cast<uint32_t*>(acat + m * 3 * D + bp * 2 * D + (int64_t)g * Dg)[wi] = v;
+    const __nv_bfloat16* src = recv + row * Dg;
+    __nv_bfloat16* dst = acat + m * 3 * D + bp * 2 * D + (int64_t)g * Dg;
+    if (v16) {
+      for (int64_t i = lane; i < Dg / 8; i += 32)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {  // Dg even (dh even): 4-byte words
+      for (int64_t i = lane; i < Dg / 2; i += 32)
+        reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+    }
   }
 }
 
@@ -449,8 +474,8 @@ int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, 
   if (Mr == 0) return VC_OK;
   bf* acat = (bf*)((char*)ws + w.acat);
   {
-    const int64_t total = x.P * 2 * Mr * (x.Dg / 2);
-    const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+    const int64_t rows = x.P * 2 * Mr;  // one warp per row
+    const int blocks = (int)std::min<int64_t>(cdiv(rows, 8), 148 * 16);
     sp_unpack2_kernel<<<blocks, 256, 0, st>>>((const bf*)recv2, acat, (int)x.P, Mr, x.Dg, x.D);
     VC_CHECK_LAUNCH();
     profile_mark(st, "sp_unpack2");
