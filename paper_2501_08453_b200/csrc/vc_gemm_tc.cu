@@ -216,7 +216,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
 // (rms(u) * w, eps 1e-6), rotates the dh/2 pairs by the token's (frame, row,
 // column) angles and stores the DP-wide head row.  V and the temporal
 // columns take the plain EPI_QKV chunk path.  (oracle/vchitect_ext_oracle.py)
-template <int DP>
+// DH: the real head dim when known at compile time (0: runtime s.dh), which
+// turns the dh guards and the RoPE axis selection into constants.
+template <int DP, int DH = 0>
 __device__ __forceinline__ void qkvn_head(const GemmTcParams& p, int64_t m, int n0, uint32_t taddr,
                                           const float* sbias) {
   const QkvScatter& s = p.qkv;
@@ -260,10 +262,11 @@ __device__ __forceinline__ void qkvn_head(const GemmTcParams& p, int64_t m, int 
   const float ss = (ss4[0] + ss4[1]) + (ss4[2] + ss4[3]);
   const int bi = b == 0 ? 0 : 1;
   const float2* w2 = reinterpret_cast<const float2*>(which == 0 ? s.qn[bi] : s.kn[bi]);  // dh even: 8-byte aligned
-  const float rs = rsqrtf(ss / (float)s.dh + 1e-6f);
+  const int dh = DH ? DH : s.dh;
+  const float rs = rsqrtf(ss / (float)dh + 1e-6f);
 #pragma unroll
   for (int i = 0; i < DP / 2; ++i)
-    if (2 * i < s.dh) {
+    if (2 * i < dh) {
       const float2 w = __ldg(w2 + i);
       v[2 * i] *= rs * w.x;
       v[2 * i + 1] *= rs * w.y;
@@ -273,13 +276,15 @@ __device__ __forceinline__ void qkvn_head(const GemmTcParams& p, int64_t m, int 
   if (!s.text_rows) {  // visual token: (frame, row, column) rotation
     const int64_t f = m / s.Lv, l = m - f * s.Lv;
     const int y = (int)(l / s.gw), x = (int)(l - (int64_t)(l / s.gw) * s.gw);
-    const int nt = s.rope_nt, nty = s.rope_nt + s.rope_ny;
+    // compile-time split when DH is known (vc_ext.cu rope_split: ny = nx = P/3)
+    const int nt = DH ? DH / 2 - 2 * (DH / 6) : s.rope_nt;
+    const int nty = DH ? DH / 2 - DH / 6 : s.rope_nt + s.rope_ny;
     const float2* pt = s.rope + f * nt;
     const float2* py = s.rope + s.rope_off_y + (int64_t)y * s.rope_ny - nt;
     const float2* px = s.rope + s.rope_off_x + (int64_t)x * s.rope_nx - nty;
 #pragma unroll
     for (int i = 0; i < DP / 2; ++i) {
-      if (2 * i < s.dh) {
+      if (2 * i < dh) {
         const float2 cs = __ldg(i < nt ? pt + i : i < nty ? py + i : px + i);
         const float a = v[2 * i], c = v[2 * i + 1];
         v[2 * i] = a * cs.x - c * cs.y;
@@ -629,12 +634,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       ptx::fence_after_sync();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
       if constexpr ((EPI & 255) == EPI_QKVN) {  // EPI = EPI_QKVN | DP << 8: head by head
-        constexpr int EDP = EPI >> 8;
+        constexpr int EDP = (EPI >> 8) & 255, EDH = EPI >> 16;
 #pragma unroll 1
         for (int hb = 0; hb < BN / EDP; ++hb) {
           const int n0 = nt * BN + hb * EDP;
           if (n0 >= p.N || mrow0 >= p.M) break;
-          qkvn_head<EDP>(p, m, n0, tbase + hb * EDP, p.bias ? sbias + hb * EDP : nullptr);
+          qkvn_head<EDP, EDH>(p, m, n0, tbase + hb * EDP, p.bias ? sbias + hb * EDP : nullptr);
         }
       } else {
         const int sp_f = EPI == EPI_QKV && m < p.M ? qkv_frame(p.qkv, m) : 0;
@@ -836,6 +841,9 @@ static int launch_gemm_tc_ext(const void* A, int64_t lda, const void* B, int64_t
   if (epi == EPI_QKVN) {
     if (dp == 64 && bn == 256) return launch_impl2<256, EPI_QKVN | (64 << 8), 1>(ta, tb, p, st);
     if (dp == 64 && bn == 128) return launch_impl2<128, EPI_QKVN | (64 << 8), 1>(ta, tb, p, st);
+    // the 2B head dim (66) specialised; other dims take the runtime-dh epilogue
+    if (dp == 80 && bn == 240 && p.qkv.dh == 66) return launch_impl2<240, EPI_QKVN | (80 << 8) | (66 << 16), 1>(ta, tb, p, st);
+    if (dp == 80 && bn == 160 && p.qkv.dh == 66) return launch_impl2<160, EPI_QKVN | (80 << 8) | (66 << 16), 1>(ta, tb, p, st);
     if (dp == 80 && bn == 240) return launch_impl2<240, EPI_QKVN | (80 << 8), 1>(ta, tb, p, st);
     if (dp == 80 && bn == 160) return launch_impl2<160, EPI_QKVN | (80 << 8), 1>(ta, tb, p, st);
     if (dp == 128 && bn == 256) return launch_impl2<256, EPI_QKVN | (128 << 8), 1>(ta, tb, p, st);
