@@ -474,7 +474,7 @@ constexpr int stages2_for() {
 template <int BN, int EPI, int EW = 4>
 constexpr size_t smem2_bytes() {  // stages + barriers + bias staging per epilogue warp (+ gate, EPI_F32G) + align
   return (size_t)stages2_for<BN>() * (BM * BK * 2 + (BN / 2) * BK * 2) + 256 + EW * 256 * 4 +
-         (EPI == EPI_F32G ? 4 * 256 * 4 : 0) + 1024;
+         (EPI == EPI_F32G ? EW * 256 * 4 : 0) + 1024;
 }
 
 // NP = CTA pairs per cluster.  NP = 2: the two pairs of a 4-CTA cluster
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     const int sub = ew >> 2;          // which of the EW / 4 warps on this quarter
     const int lane = threadIdx.x & 31;
     float* sbias = sbias_all + ew * 256;
-    float* sgate = sbias_all + EW * 256 + q * 256;  // EPI_F32G only (smem2_bytes)
+    float* sgate = sbias_all + EW * 256 + ew * 256;  // EPI_F32G only (smem2_bytes)
     const uint32_t tempty_leader = ptx::mapa_shared(ptx::smem_u32(tempty), (uint32_t)(2 * pair));
     int local = 0;
     for (int t = cluster; t < tiles; t += nclusters, ++local) {
@@ -826,6 +826,24 @@ int gemm_tc_pick_bn(int N, int np) {
 // starts each launch at a segment base).
 static int launch_gemm_tc_ext(const void* A, int64_t lda, const void* B, int64_t ldb,
                               const GemmTcParams& p, int epi, cudaStream_t st) {
+  if (epi == EPI_F32G && p.M > BM) {
+    // gated residual (long-K GEMMs: O projection, FFN down): two CTA pairs per
+    // cluster sharing A, like the O GEMM of the reference-semantics block
+    const int bn2 = gemm_tc_pick_bn(p.N, 2);
+    if (cdiv(p.N, bn2) >= 2) {
+      CUtensorMap ta, tb;
+      VC_TRY(make_tmap_2d_bf16(&ta, A, p.K, p.M, lda * 2, BK, BM / 2, CU_TENSOR_MAP_SWIZZLE_128B));
+      VC_TRY(make_tmap_2d_bf16(&tb, B, p.K, p.N, ldb * 2, BK, bn2 / 2, CU_TENSOR_MAP_SWIZZLE_128B));
+      switch (bn2) {
+        case 256: return launch_impl2<256, EPI_F32G, 2>(ta, tb, p, st);
+        case 240: return launch_impl2<240, EPI_F32G, 2>(ta, tb, p, st);
+        case 208: return launch_impl2<208, EPI_F32G, 2>(ta, tb, p, st);
+        case 176: return launch_impl2<176, EPI_F32G, 2>(ta, tb, p, st);
+        case 160: return launch_impl2<160, EPI_F32G, 2>(ta, tb, p, st);
+        default: return launch_impl2<128, EPI_F32G, 2>(ta, tb, p, st);
+      }
+    }
+  }
   const int dp = epi == EPI_QKVN ? p.qkv.pad.DP : 16;
   int bn = 0;
   int64_t best = INT64_MAX;
