@@ -158,7 +158,16 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
         if (bp == 0) dst = (which == 0 ? a.qsp : a.ksp) + tok * rowlen;
         else dst = which == 0 ? a.qfs + tok * rowlen : a.kfs + (a.Lt + tok) * rowlen;
         uint4* d4 = reinterpret_cast<uint4*>(dst);
-        for (int i = lane; i < rowlen / 8; i += 32) d4[i] = s4[i];
+        // all of the row's loads first (up to 8 x 16 bytes per lane in flight), then the stores
+        const int n = rowlen / 8;
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (lane + 32 * u < n) v[u] = s4[lane + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (lane + 32 * u < n) d4[lane + 32 * u] = v[u];
+        for (int i = lane + 256; i < n; i += 32) d4[i] = s4[i];  // rows longer than 256 x 16 bytes
       }
       continue;
     }
