@@ -188,11 +188,16 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
       int64_t ld, key;
       if (bp == 0) { base = a.vtsp + (int64_t)f * a.Hg * a.DP * a.Lv_ld; ld = a.Lv_ld; key = l; }
       else { base = a.vtfs; ld = a.Lk_ld; key = a.Lt + tok; }
-      for (int i = 0; i < rowlen / 8; ++i) {
-        const uint4 v = reinterpret_cast<const uint4*>(src)[i];
-        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+      const int n = rowlen / 8;  // DP is a multiple of 16: n is even
+      for (int i = 0; i < n; i += 2) {  // two 16-byte loads in flight before the 16 stores
+        const uint4 v0 = reinterpret_cast<const uint4*>(src)[i];
+        const uint4 v1 = reinterpret_cast<const uint4*>(src)[i + 1];
+        const __nv_bfloat16* e0 = reinterpret_cast<const __nv_bfloat16*>(&v0);
+        const __nv_bfloat16* e1 = reinterpret_cast<const __nv_bfloat16*>(&v1);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) base[(int64_t)(i * 8 + k) * ld + key] = e[k];  // row hl*DP+d of Vt
+        for (int k = 0; k < 8; ++k) base[(int64_t)(i * 8 + k) * ld + key] = e0[k];  // row hl*DP+d of Vt
+#pragma unroll
+        for (int k = 0; k < 8; ++k) base[(int64_t)(i * 8 + 8 + k) * ld + key] = e1[k];
       }
     }
   }
