@@ -53,11 +53,14 @@ size_t bf16_workspace_acat_offset(int64_t F, int64_t Lv, int64_t Lt, int64_t D, 
   return ws_layout(F, Lv, Lt, D, H).acat;
 }
 
-int bf16_launch_count(int64_t, int64_t, int64_t Lt, int64_t, int64_t) { return Lt > 0 ? 7 : 6; }
+int bf16_launch_count(int64_t, int64_t, int64_t Lt, int64_t D, int64_t H) {
+  return (Lt > 0 ? 7 : 6) + (qkv_compact_ok(D, H) ? 2 : 0);  // + the two V^T pad fills
+}
 
 int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, const void* wqkv,
                        const float* bias, const void* wo, const float* x, const float* prompt,
-                       float* out, int add_residual, char* ws, cudaStream_t st, const ExtArgs* ext) {
+                       float* out, int add_residual, char* ws, cudaStream_t st, const ExtArgs* ext,
+                       const void* wqkv_c, const float* bias_c) {
   const WsBf16 wl = ws_layout(F, Lv, Lt, D, H);
   const int64_t Nv = F * Lv, dh = D / H;
   if (wl.DP == 0) { set_error("head dim %lld unsupported on the tensor-core path", (long long)dh); return VC_ENOTSUP; }
@@ -70,7 +73,11 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   else VC_TRY(launch_ln_rows<bf>(x, Nv, prompt, Lt, (int)D, xhat, st));
   profile_mark(st, "ln");
 
-  const QkvPad pad = qkv_pad_layout(D, H);
+  // the compact column space (dh 66; no padding columns in the GEMM) unless the
+  // extension's head-aligned QK-norm epilogue needs the padded one
+  const bool compact = !ext && wqkv_c && bias_c && qkv_compact_ok(D, H);
+  if (compact) { wqkv = wqkv_c; bias = bias_c; }
+  const QkvPad pad = compact ? qkv_compact_layout(D, H) : qkv_pad_layout(D, H);
   QkvScatter sc{};
   sc.pad = pad; sc.D = D; sc.Lv = Lv; sc.Lt = Lt; sc.H = (int)H;
   sc.sp = BranchOut{(bf*)(ws + wl.qsp), (bf*)(ws + wl.ksp), (bf*)(ws + wl.vtsp), wl.Lv_ld};
@@ -94,7 +101,14 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     GemmTcParams g{};
     g.M = Nv; g.N = (int)pad.Npad; g.K = (int)D; g.bias = bias;
     g.qkv = sc; g.qkv.n_base = 0; g.qkv.text_rows = 0;
-    VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_QKV, st));
+    // compact: 256-column tiles (the least-padding pick would be 176, whose
+    // smaller tiles cost more than the 80 padding columns of 256)
+    static const int qkv_bn = getenv("VC_QKV_BN") ? atoi(getenv("VC_QKV_BN")) : 256;  // A/B
+    VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_QKV, st, compact ? qkv_bn : 0));
+  }
+  if (compact) {  // V^T rows dh..DP-1 (ones column, zeros) the compact GEMM does not write
+    VC_TRY(launch_fill_vt_pad(sc.sp.vt, F * H, (int)wl.DP, (int)dh, wl.Lv_ld, Lv, st));
+    VC_TRY(launch_fill_vt_pad(sc.fs.vt, H, (int)wl.DP, (int)dh, wl.Lk_ld, Lt + Nv, st));
   }
   profile_mark(st, "qkv_gemm");
   if (Lt > 0) {  // prompt rows: only the full-sequence K and V segments

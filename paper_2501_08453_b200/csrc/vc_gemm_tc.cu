@@ -168,7 +168,30 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
     const int seg = (int)q.SEG;
     const int which = r / seg;
     const int jj = r - which * seg;
-    const int hg = jj / q.DP, d0 = jj - hg * q.DP;  // 16 | DP: the chunk is inside head hg
+    if (q.compact && jj >= q.MAIN) {  // compact tail chunk: (h, 64), (h, 65) pairs of 8 heads (mode 0)
+      const BranchOut& bo = b == 0 ? s.sp : s.fs;
+      int64_t qrow, krow, seq, key;
+      qkv_rows(s, b, m, sp_f >= 0 ? sp_f : qkv_frame(s, m), qrow, krow, seq, key);
+      const int h0 = (jj - (int)q.MAIN) >> 1;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int h = h0 + i - s.head_base;
+        if (h >= s.H) break;
+        if (which < 2) {  // d 64, 65 and the zero padding 66..79 of the head slot
+          const int64_t row = which == 0 ? qrow : krow;
+          if (row < 0) continue;
+          uint4* o = reinterpret_cast<uint4*>((which == 0 ? bo.q : bo.k) + (row * s.H + h) * q.DP + 64);
+          o[0] = make_uint4(pack_bf16x2(v[2 * i], v[2 * i + 1]), 0u, 0u, 0u);
+          o[1] = make_uint4(0u, 0u, 0u, 0u);
+        } else {  // V^T rows 64, 65 (rows 66..79: fill_vt_pad_kernel)
+          __nv_bfloat16* o = bo.vt + ((seq * s.H + h) * q.DP + 64) * bo.ld_key + key;
+          o[0] = __float2bfloat16_rn(v[2 * i]);
+          o[bo.ld_key] = __float2bfloat16_rn(v[2 * i + 1]);
+        }
+      }
+      return;
+    }
+    const int hg = jj / q.HW, d0 = jj - hg * q.HW;  // 16 | HW: the chunk is inside head hg
     if (s.mode == 1) {  // sequence-parallel send layout, branch-major: [b'][g][which][m][Hg][DP]
       const int g = hg / s.Hg, hl = hg - g * s.Hg;
       const int P = s.H / s.Hg;

@@ -53,11 +53,24 @@ int launch_unembed(const float* x, const float* w_out, float* eps, int F, int h,
 // head and is stored as one contiguous 32-byte run of the attention layout;
 // the temporal segment is the plain 3D columns.  Segment order:
 //   sp.q sp.k sp.v | tm (3D) | fs.q fs.k fs.v
+//
+// Compact variant (dh = 66, the 2B head dim; single-GPU block only): the GEMM
+// computes no padding columns.  Each sp / fs segment is
+//   [head h: columns 0..63, 64-column runs, h = 0..H-1] [tail: (h, 64), (h, 65) pairs]
+// (HW = 64 columns per head in the main part, MAIN = 64 H; the tail packs 8
+// heads per 16-column chunk, rounded up to 16).  The destination layouts keep
+// the DP = 80 head slots: the tail chunk writes d = 64..79 of Q/K rows (the
+// real pair and the zero padding) and V^T rows 64, 65; V^T rows 66..79 (the
+// ones column and zeros) are written by fill_vt_pad_kernel.  12% fewer MMA
+// columns than the padded space for the same stores.
 struct QkvPad {
-  int32_t DP;       // padded head dim (64, 80 or 128)
-  int64_t SEG;      // H*DP
+  int32_t DP;       // head slot of the destination layouts (64, 80 or 128)
+  int64_t SEG;      // columns per sp / fs Q, K or V segment: H*DP (padded) or MAIN + tail (compact)
   int64_t TMSEG;    // round_up(3D, 16)
   int64_t Npad;     // 6*SEG + TMSEG
+  int32_t HW;       // columns per head in the main part: DP (padded) or 64 (compact)
+  int32_t compact;  // 1: compact column space (tail chunks after MAIN)
+  int64_t MAIN;     // H*HW
   __host__ __device__ int64_t fs_base() const { return 3 * SEG + TMSEG; }
 };
 inline int qkv_head_pad(int64_t dh) { return dh <= 64 ? 64 : dh <= 80 ? 80 : dh <= 128 ? 128 : 0; }
@@ -67,14 +80,33 @@ inline QkvPad qkv_pad_layout(int64_t D, int64_t H) {
   q.SEG = H * q.DP;
   q.TMSEG = (3 * D + 15) / 16 * 16;
   q.Npad = 6 * q.SEG + q.TMSEG;
+  q.HW = q.DP;
+  q.compact = 0;
+  q.MAIN = q.SEG;
+  return q;
+}
+inline bool qkv_compact_ok(int64_t D, int64_t H) { return H > 0 && D % H == 0 && D / H == 66; }
+inline QkvPad qkv_compact_layout(int64_t D, int64_t H) {
+  if (!qkv_compact_ok(D, H)) return qkv_pad_layout(D, H);
+  QkvPad q = qkv_pad_layout(D, H);
+  q.HW = 64;
+  q.compact = 1;
+  q.MAIN = H * 64;
+  q.SEG = q.MAIN + (2 * H + 15) / 16 * 16;
+  q.Npad = 6 * q.SEG + q.TMSEG;
   return q;
 }
 
 int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int H, bool bf16,
-                cudaStream_t st);
-// Byte offsets inside the packed weight buffer (vc_block.cu).
+                cudaStream_t st, void* wqkv_c = nullptr, float* bias_c = nullptr);
+// Byte offsets inside the packed weight buffer (vc_block.cu).  wqkv_c /
+// bias_c: the compact QKV column space (qkv_compact_layout; == wqkv / bias
+// when the shape has none).
 void packed_offsets(int64_t D, int64_t H, bool bf16, size_t* wqkv, size_t* bias, size_t* wo,
-                    size_t* total);
+                    size_t* total, size_t* wqkv_c = nullptr, size_t* bias_c = nullptr);
+// V^T rows [dh, DP) of the compact layout: the ones column (row dh) and zeros
+int launch_fill_vt_pad(__nv_bfloat16* vt, int64_t nslots, int DP, int dh, int64_t ld, int64_t keys,
+                       cudaStream_t st);
 
 // stage profiler (vc_profile.cu)
 bool profile_on();
@@ -105,7 +137,8 @@ struct ExtArgs {
 int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, const void* wqkv,
                        const float* bias, const void* wo, const float* x, const float* prompt,
                        float* out, int add_residual, char* ws, cudaStream_t st,
-                       const ExtArgs* ext = nullptr);
+                       const ExtArgs* ext = nullptr, const void* wqkv_c = nullptr,
+                       const float* bias_c = nullptr);
 // bytes of the bf16 block workspace region holding the O-GEMM A operand
 // (acat, [Nv][3D] bf16), reused by the extension as the FFN hidden when Dff <= 3D
 size_t bf16_workspace_acat_offset(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H);

@@ -314,6 +314,14 @@ __device__ __forceinline__ bool qkv_source(int64_t n, int D, int H, bool padded,
     which = (int)(j / D); c = (int)(j % D);
     return true;
   } else { b = 2; const int64_t r = n - q.fs_base(); which = (int)(r / q.SEG); j = r % q.SEG; }
+  if (q.compact) {  // [h: d 0..63] x H, then the (h, 64), (h, 65) tail pairs (vc_kernels.h)
+    int h, d;
+    if (j < q.MAIN) { h = (int)(j / q.HW); d = (int)(j % q.HW); }
+    else { const int t = (int)(j - q.MAIN); h = t / (dh - q.HW); d = q.HW + t % (dh - q.HW); }
+    if (h >= H) { c = -2; return false; }
+    c = h * dh + d;
+    return true;
+  }
   const int h = (int)(j / q.DP), d = (int)(j % q.DP);
   if (h >= H || d >= dh) {
     c = (h < H && d == dh) ? -1 : -2;  // -1: first V pad column (the ones column, see below)
@@ -327,6 +335,7 @@ __device__ __forceinline__ bool qkv_source(int64_t n, int D, int H, bool padded,
 // (zero weights, bias 1): the P.V MMA then accumulates the softmax row sum
 // in O[:, dh] for free, in the same bf16 P the numerator uses.
 __device__ __forceinline__ bool is_ones_column(int64_t n, int D, int H, QkvPad q) {
+  if (q.compact) return false;  // compact: fill_vt_pad_kernel writes the ones row
   int b, which, c;
   if (qkv_source(n, D, H, true, q, b, which, c)) return false;
   return b != 1 && which == 2 && c == -1;
@@ -380,7 +389,7 @@ __global__ void pack_o_kernel(const float* __restrict__ raw, T* __restrict__ wo,
 }
 
 int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int H, bool bf16,
-                cudaStream_t st) {
+                cudaStream_t st, void* wqkv_c, float* bias_c) {
   const int blocks = 148 * 8;
   const QkvPad q = qkv_pad_layout(D, H);
   const int64_t N = bf16 ? q.Npad : 9 * (int64_t)D;
@@ -388,11 +397,43 @@ int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int 
     if (q.DP == 0) { set_error("head dim %d unsupported on the bf16 path", D / H); return VC_ENOTSUP; }
     pack_qkv_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wqkv, D, H, N, q);
     pack_o_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wo, D);
+    if (wqkv_c && bias_c && qkv_compact_ok(D, H)) {
+      const QkvPad qc = qkv_compact_layout(D, H);
+      pack_qkv_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wqkv_c, D, H, qc.Npad, qc);
+      pack_bias_kernel<<<(unsigned)cdiv(qc.Npad, 128), 128, 0, st>>>(raw, bias_c, D, H, qc.Npad, true, qc);
+    }
   } else {
     pack_qkv_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wqkv, D, H, N, q);
     pack_o_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wo, D);
   }
   pack_bias_kernel<<<(unsigned)cdiv(N, 128), 128, 0, st>>>(raw, bias, D, H, N, bf16, q);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
+// V^T rows [dh, DP) of every (sequence, head) slot for keys [0, keys): the
+// ones column (row dh) and zeros.  The compact QKV GEMM writes rows < dh only.
+__global__ void fill_vt_pad_kernel(__nv_bfloat16* __restrict__ vt, int64_t nslots, int DP, int dh, int64_t ld,
+                                   int64_t keys) {
+  const int rows = DP - dh;
+  const int64_t kw = (keys + 1) / 2;  // 4-byte words per row (ld even)
+  const int64_t total = nslots * rows * kw;
+  const __nv_bfloat162 one = __floats2bfloat162_rn(1.f, 1.f), zero = __floats2bfloat162_rn(0.f, 0.f);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = e % kw;
+    const int64_t sr = e / kw;
+    const int r = (int)(sr % rows);
+    const int64_t slot = sr / rows;
+    reinterpret_cast<__nv_bfloat162*>(vt + (slot * DP + dh + r) * ld)[w] = r == 0 ? one : zero;
+  }
+}
+
+int launch_fill_vt_pad(__nv_bfloat16* vt, int64_t nslots, int DP, int dh, int64_t ld, int64_t keys,
+                       cudaStream_t st) {
+  if (nslots <= 0 || keys <= 0 || dh >= DP) return VC_OK;
+  if (ld % 2) { set_error("V^T pitch must be even"); return VC_EINVAL; }
+  const int64_t total = nslots * (DP - dh) * ((keys + 1) / 2);
+  fill_vt_pad_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 16), 256, 0, st>>>(vt, nslots, DP, dh, ld, keys);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }

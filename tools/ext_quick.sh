@@ -1,5 +1,12 @@
 cd $GRAFT_REPO_ROOT
-timeout -s KILL 600 python -m pytest tests/test_gpu_sp.py -x -q > gpurun_out/sp_tests.log 2>&1; echo "rc=$?" >> gpurun_out/sp_tests.log
-export RANK=0 WORLD_SIZE=1 LOCAL_RANK=0 MASTER_ADDR=127.0.0.1 MASTER_PORT=29655
-timeout -s KILL 300 python bench.py --sp --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/sp1_plain.log 2>&1; echo "rc=$?" >> gpurun_out/sp1_plain.log
-timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/sp1_launches.csv python bench.py --sp --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/sp1_ncu.log 2>&1; echo "rc=$?" >> gpurun_out/sp1_ncu.log
+for i in 1 2; do
+for bn in 256 240 208; do
+VC_QKV_BN=$bn timeout -s KILL 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/c_b.log 2>&1
+python - $bn <<'PY'
+import json,sys
+for l in open("gpurun_out/c_b.log"):
+    if l.startswith("{"):
+        d=json.loads(l); s=d["block"]["stage_ms"]
+        print("bn", sys.argv[1], "ms %.3f"%d["ms_per_step"], "qkv %.4f"%s["qkv_gemm"])
+PY
+done; done
