@@ -27,6 +27,12 @@ struct AttnTcParams {
   int64_t col_off;
   int64_t out_seq_rows;
   SpOutMap spo;
+  // 0: head h at col_off + h*dh (dh columns).  Else head h at col_off +
+  // h*head_slot, written as whole 16-column chunks with zeros past dh (full
+  // 32-byte sectors: partial-sector row stores cost ~14% of a 1350-key
+  // attention, profiles/r01/attn_study); the O GEMM's weights have zero rows
+  // for the slot padding.
+  int32_t head_slot;
 };
 
 // Two-query-tile (ping-pong) kernel for DP <= 80 (vc_attn_tc2.cu).

@@ -120,7 +120,9 @@ __device__ __forceinline__ void store_p(uint32_t p_tile, int row, const float (&
 // Output row of query qi (sequence seq, head h): plain [seq * out_seq_rows + qi]
 // rows, or the sequence-parallel branch-major send blocks (spo).
 __device__ __forceinline__ __nv_bfloat16* out_row(const AttnTcParams& p, int qi, int seq, int h) {
-  if (p.spo.P == 0) return p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off + (int64_t)h * p.dh;
+  if (p.spo.P == 0)
+    return p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off +
+           (int64_t)h * (p.head_slot ? p.head_slot : p.dh);
   const int f = p.spo.branch == 0 ? seq : qi / p.spo.Lv;
   const int lpos = p.spo.branch == 0 ? qi : qi - f * p.spo.Lv;
   int r = 0;
@@ -135,6 +137,28 @@ __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr
                                           int h) {
   const float inv = 1.f / l;
   __nv_bfloat16* orow = qi < p.Lq ? out_row(p, qi, seq, h) : nullptr;
+  if (p.head_slot) {  // whole 16-column chunks (zeros past dh): full-sector 16-byte stores
+#pragma unroll
+    for (int c = C0; c < C1; ++c) {
+      uint32_t r[16];
+      ptx::tmem_ld16(o_addr + c * 16, r);
+      ptx::tmem_ld_wait();
+      if (orow) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float a = (c * 16 + 2 * i < p.dh) ? __uint_as_float(r[2 * i]) * inv : 0.f;
+          const float b = (c * 16 + 2 * i + 1 < p.dh) ? __uint_as_float(r[2 * i + 1]) * inv : 0.f;
+          __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+          w[i] = *reinterpret_cast<uint32_t*>(&t);
+        }
+        uint4* o = reinterpret_cast<uint4*>(orow + c * 16);
+        o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+    }
+    return;
+  }
 #ifdef VC_ATTN_TRACE
   if (!p.out) orow = nullptr;  // trace builds: time the kernel without its output stores
 #endif

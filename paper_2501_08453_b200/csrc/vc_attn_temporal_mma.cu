@@ -49,7 +49,7 @@ template <int KS, int NT, bool VEC16>
 __global__ void __launch_bounds__(kWarps * 32)
     temporal_mma_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int64_t D,
                         __nv_bfloat16* __restrict__ o, int64_t ldo, int F, int Lv, int H, int dh,
-                        float scale_log2) {
+                        float scale_log2, int hs) {
   constexpr int KPAD = 16 * KS + 8;  // smem row pitch (elements): conflict-free ldmatrix
   __shared__ __align__(16) __nv_bfloat16 sK[kWarps][16][KPAD];
   __shared__ __align__(16) __nv_bfloat16 sV[kWarps][16][KPAD];
@@ -189,12 +189,14 @@ __global__ void __launch_bounds__(kWarps * 32)
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   const float i0 = 1.f / l0, i1 = 1.f / l1;
   const int fr0 = f0 + g, fr1 = f0 + g + 8;
-  __nv_bfloat16* o0 = o + ((int64_t)fr0 * Lv + l) * ldo + col0;
-  __nv_bfloat16* o1 = o + ((int64_t)fr1 * Lv + l) * ldo + col0;
+  // hs: output head stride (dh, or a padded slot whose columns past dh get
+  // the zeros oacc holds there: V's padding is zero-filled in smem)
+  __nv_bfloat16* o0 = o + ((int64_t)fr0 * Lv + l) * ldo + (int64_t)h * hs;
+  __nv_bfloat16* o1 = o + ((int64_t)fr1 * Lv + l) * ldo + (int64_t)h * hs;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const int c = 8 * j + 2 * t;
-    if (c < dh) {
+    if (c < hs) {
       if (fr0 < F) *reinterpret_cast<__nv_bfloat162*>(o0 + c) = __floats2bfloat162_rn(oacc[j][0] * i0, oacc[j][1] * i0);
       if (fr1 < F) *reinterpret_cast<__nv_bfloat162*>(o1 + c) = __floats2bfloat162_rn(oacc[j][2] * i1, oacc[j][3] * i1);
     }
@@ -203,16 +205,16 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 template <int KS, int NT>
 int launch_ks(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo, int F, int Lv,
-              int H, int dh, cudaStream_t st) {
+              int H, int dh, cudaStream_t st, int hs) {
   const int64_t items = (int64_t)Lv * H * ((F + 15) / 16);
   const int64_t blocks = cdiv(items, kWarps);
   if (blocks > 2147483647) { set_error("temporal grid too large"); return VC_ENOTSUP; }
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)dh));
   const bool vec16 = dh % 8 == 0 && ld % 8 == 0 && D % 8 == 0 && ((uintptr_t)qkv % 16) == 0;
   if (vec16)
-    temporal_mma_kernel<KS, NT, true><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2);
+    temporal_mma_kernel<KS, NT, true><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs);
   else
-    temporal_mma_kernel<KS, NT, false><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2);
+    temporal_mma_kernel<KS, NT, false><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
@@ -220,22 +222,27 @@ int launch_ks(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o,
 }  // namespace
 
 int launch_temporal_mma(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo, int F,
-                        int Lv, int H, int dh, cudaStream_t st) {
+                        int Lv, int H, int dh, cudaStream_t st, int head_slot) {
   if (F <= 0 || Lv <= 0) return VC_OK;
+  const int hs = head_slot ? head_slot : dh;
+  if (hs < dh || (head_slot && head_slot > 16 * ((dh + 15) / 16))) {
+    set_error("temporal attention head slot %d does not fit dh %d", head_slot, dh);
+    return VC_EINVAL;
+  }
   if (dh % 2 != 0 || dh > 128 || (ld % 2) || (D % 2) || (ldo % 2)) {
     set_error("tensor-core temporal attention needs an even head dim <= 128 (dh %d)", dh);
     return VC_ENOTSUP;
   }
   const int ks = (dh + 15) / 16;
   switch (ks) {
-    case 1: return launch_ks<1, 2>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
-    case 2: return launch_ks<2, 4>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
-    case 3: return launch_ks<3, 6>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
-    case 4: return launch_ks<4, 8>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
-    case 5: return launch_ks<5, 10>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
-    case 6: return launch_ks<6, 12>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
-    case 7: return launch_ks<7, 14>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
-    default: return launch_ks<8, 16>(qkv, ld, D, o, ldo, F, Lv, H, dh, st);
+    case 1: return launch_ks<1, 2>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    case 2: return launch_ks<2, 4>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    case 3: return launch_ks<3, 6>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    case 4: return launch_ks<4, 8>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    case 5: return launch_ks<5, 10>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    case 6: return launch_ks<6, 12>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    case 7: return launch_ks<7, 14>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    default: return launch_ks<8, 16>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
   }
 }
 

@@ -77,10 +77,10 @@ static int check_shape(const vc_block_shape* s, Dims* d) {
 
 // ---- packed weight layout --------------------------------------------------
 struct PackedLayout {
-  size_t wqkv, bias, wo, total, wqkv_c, bias_c;
+  size_t wqkv, bias, wo, total, wqkv_c, bias_c, wo_s;
 };
 void packed_offsets(int64_t D, int64_t H, bool bf16, size_t* wqkv, size_t* bias, size_t* wo,
-                    size_t* total, size_t* wqkv_c, size_t* bias_c) {
+                    size_t* total, size_t* wqkv_c, size_t* bias_c, size_t* wo_s) {
   const size_t es = bf16 ? 2 : 4;
   // bf16: head-padded QKV column space (vc_kernels.h QkvPad); fp32: plain 9D
   const int64_t nq = bf16 ? qkv_pad_layout(D, H).Npad : 9 * D;
@@ -88,19 +88,21 @@ void packed_offsets(int64_t D, int64_t H, bool bf16, size_t* wqkv, size_t* bias,
   *bias = align_up(*wqkv + (size_t)nq * D * es, 1024);
   *wo = align_up(*bias + (size_t)nq * 4, 1024);
   *total = align_up(*wo + (size_t)3 * D * D * es, 1024);
-  size_t wc = *wqkv, bc = *bias;
-  if (bf16 && qkv_compact_ok(D, H)) {  // + the compact QKV space the single-GPU block runs on
+  size_t wc = *wqkv, bc = *bias, ws = *wo;
+  if (bf16 && qkv_compact_ok(D, H)) {  // + the compact QKV space and the head-slot Wo of the single-GPU block
     const int64_t nc = qkv_compact_layout(D, H).Npad;
     wc = *total;
     bc = align_up(wc + (size_t)nc * D * es, 1024);
-    *total = align_up(bc + (size_t)nc * 4, 1024);
+    ws = align_up(bc + (size_t)nc * 4, 1024);
+    *total = align_up(ws + (size_t)3 * H * qkv_pad_layout(D, H).DP * D * es, 1024);
   }
   if (wqkv_c) *wqkv_c = wc;
   if (bias_c) *bias_c = bc;
+  if (wo_s) *wo_s = ws;
 }
 static PackedLayout packed_layout(const Dims& d) {
   PackedLayout p;
-  packed_offsets(d.D, d.H, d.bf16, &p.wqkv, &p.bias, &p.wo, &p.total, &p.wqkv_c, &p.bias_c);
+  packed_offsets(d.D, d.H, d.bf16, &p.wqkv, &p.bias, &p.wo, &p.total, &p.wqkv_c, &p.bias_c, &p.wo_s);
   return p;
 }
 
@@ -243,7 +245,8 @@ int vc_pack_block_weights(const vc_block_shape* shape, const float* raw_dev, voi
   const PackedLayout pl = packed_layout(d);
   char* p = (char*)packed_dev;
   return launch_pack(raw_dev, p + pl.wqkv, (float*)(p + pl.bias), p + pl.wo, (int)d.D, (int)d.H,
-                     d.bf16, (cudaStream_t)stream, pl.wqkv_c != pl.wqkv ? p + pl.wqkv_c : nullptr, pl.wqkv_c != pl.wqkv ? (float*)(p + pl.bias_c) : nullptr);
+                     d.bf16, (cudaStream_t)stream, pl.wqkv_c != pl.wqkv ? p + pl.wqkv_c : nullptr, pl.wqkv_c != pl.wqkv ? (float*)(p + pl.bias_c) : nullptr,
+                     pl.wqkv_c != pl.wqkv ? p + pl.wo_s : nullptr);
 }
 
 int vc_block_forward(const vc_block_shape* shape, const void* packed_dev, const float* visual_dev,
@@ -269,7 +272,7 @@ int vc_block_forward(const vc_block_shape* shape, const void* packed_dev, const 
     rc = block_forward_bf16(d.F, d.Lv, d.Lt, d.D, d.H, p + pl.wqkv, (const float*)(p + pl.bias),
                             p + pl.wo, visual_dev, prompt_dev, out_dev, add_residual,
                             (char*)workspace_dev, st, nullptr, cpt ? p + pl.wqkv_c : nullptr,
-                            cpt ? (const float*)(p + pl.bias_c) : nullptr);
+                            cpt ? (const float*)(p + pl.bias_c) : nullptr, cpt ? p + pl.wo_s : nullptr);
   } else {
     rc = block_forward_f32(d, (const char*)packed_dev, visual_dev, prompt_dev, out_dev,
                            add_residual, (char*)workspace_dev, st);

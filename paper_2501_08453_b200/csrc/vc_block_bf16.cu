@@ -39,7 +39,8 @@ WsBf16 ws_layout(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
   w.qfs = o; o = aup(o + (size_t)Nv * qk);
   w.kfs = o; o = aup(o + (size_t)(Lt + Nv) * qk);
   w.vtfs = o; o = aup(o + (size_t)H * w.DP * w.Lk_ld * 2);
-  w.acat = o; o = aup(o + (size_t)Nv * 3 * D * 2);
+  // [Nv][3D], or [Nv][3][H][DP] in the head-slot layout (DP >= dh)
+  w.acat = o; o = aup(o + (size_t)Nv * 3 * std::max<int64_t>(D, H * w.DP) * 2);
   w.total = o;
   return w;
 }
@@ -60,7 +61,7 @@ int bf16_launch_count(int64_t, int64_t, int64_t Lt, int64_t D, int64_t H) {
 int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, const void* wqkv,
                        const float* bias, const void* wo, const float* x, const float* prompt,
                        float* out, int add_residual, char* ws, cudaStream_t st, const ExtArgs* ext,
-                       const void* wqkv_c, const float* bias_c) {
+                       const void* wqkv_c, const float* bias_c, const void* wo_s) {
   const WsBf16 wl = ws_layout(F, Lv, Lt, D, H);
   const int64_t Nv = F * Lv, dh = D / H;
   if (wl.DP == 0) { set_error("head dim %lld unsupported on the tensor-core path", (long long)dh); return VC_ENOTSUP; }
@@ -120,21 +121,27 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     profile_mark(st, "text_kv_gemm");
   }
   const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)dh));
+  // O-GEMM A operand: the three branches' outputs [Nv][3D], or, with the
+  // head-slot Wo (dh 66), [Nv][3][H][DP] written as whole 16-byte sectors
+  const int slot = (!ext && wo_s) ? (int)wl.DP : 0;
+  if (slot) wo = wo_s;
+  const int64_t bw = slot ? H * slot : D;  // columns per branch in acat
+  const int64_t lda = 3 * bw;
   {
     AttnTcParams a{};
     a.Lq = (int)Lv; a.Lk = (int)Lv; a.H = (int)H; a.dh = (int)dh;
     a.n_bias = 0; a.bias_log2 = 0.f; a.scale_log2 = scale_log2;
-    a.out = acat; a.ld_out = 3 * D; a.col_off = 0; a.out_seq_rows = Lv;
+    a.out = acat; a.ld_out = lda; a.col_off = 0; a.out_seq_rows = Lv; a.head_slot = slot;
     VC_TRY(launch_attn_tc(a, sc.sp.q, sc.sp.k, sc.sp.vt, (int)F, Lv, Lv, wl.Lv_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_spatial");
-  VC_TRY(launch_temporal_mma(tm, 3 * D, D, acat + D, 3 * D, (int)F, (int)Lv, (int)H, (int)dh, st));
+  VC_TRY(launch_temporal_mma(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, st, slot));
   profile_mark(st, "attn_temporal");
   {
     AttnTcParams a{};
     a.Lq = (int)Nv; a.Lk = (int)(Lt + Nv); a.H = (int)H; a.dh = (int)dh;
     a.n_bias = (int)Lt; a.bias_log2 = (float)log2((double)F); a.scale_log2 = scale_log2;
-    a.out = acat; a.ld_out = 3 * D; a.col_off = 2 * D; a.out_seq_rows = 0;
+    a.out = acat; a.ld_out = lda; a.col_off = 2 * bw; a.out_seq_rows = 0; a.head_slot = slot;
     VC_TRY(launch_attn_tc(a, sc.fs.q, sc.fs.k, sc.fs.vt, 1, Nv, Lt + Nv, wl.Lk_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_fullseq");
@@ -162,9 +169,9 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   }
   {
     GemmTcParams g{};
-    g.M = Nv; g.N = (int)D; g.K = (int)(3 * D);
+    g.M = Nv; g.N = (int)D; g.K = (int)lda;
     g.out_f32 = out; g.ldo = D; g.R = add_residual ? x : nullptr; g.ldr = D;
-    VC_TRY(launch_gemm_tc(acat, 3 * D, wo, 3 * D, g, EPI_F32, st));
+    VC_TRY(launch_gemm_tc(acat, lda, wo, lda, g, EPI_F32, st));
   }
   profile_mark(st, "oproj_gemm");
   return VC_OK;

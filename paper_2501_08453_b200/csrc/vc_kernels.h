@@ -25,7 +25,7 @@ int launch_temporal_attn(const T* qkv, int64_t ld, int64_t D, OutT* o, int64_t l
 
 // bf16 temporal branch on warp-level tensor-core MMAs (vc_attn_temporal_mma.cu)
 int launch_temporal_mma(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo,
-                        int F, int Lv, int H, int dh, cudaStream_t st);
+                        int F, int Lv, int H, int dh, cudaStream_t st, int head_slot = 0);
 
 template <typename OutT>
 int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,
@@ -98,12 +98,13 @@ inline QkvPad qkv_compact_layout(int64_t D, int64_t H) {
 }
 
 int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int H, bool bf16,
-                cudaStream_t st, void* wqkv_c = nullptr, float* bias_c = nullptr);
+                cudaStream_t st, void* wqkv_c = nullptr, float* bias_c = nullptr, void* wo_s = nullptr);
 // Byte offsets inside the packed weight buffer (vc_block.cu).  wqkv_c /
 // bias_c: the compact QKV column space (qkv_compact_layout; == wqkv / bias
 // when the shape has none).
 void packed_offsets(int64_t D, int64_t H, bool bf16, size_t* wqkv, size_t* bias, size_t* wo,
-                    size_t* total, size_t* wqkv_c = nullptr, size_t* bias_c = nullptr);
+                    size_t* total, size_t* wqkv_c = nullptr, size_t* bias_c = nullptr,
+                    size_t* wo_s = nullptr);
 // V^T rows [dh, DP) of the compact layout: the ones column (row dh) and zeros
 int launch_fill_vt_pad(__nv_bfloat16* vt, int64_t nslots, int DP, int dh, int64_t ld, int64_t keys,
                        cudaStream_t st);
@@ -138,7 +139,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
                        const float* bias, const void* wo, const float* x, const float* prompt,
                        float* out, int add_residual, char* ws, cudaStream_t st,
                        const ExtArgs* ext = nullptr, const void* wqkv_c = nullptr,
-                       const float* bias_c = nullptr);
+                       const float* bias_c = nullptr, const void* wo_s = nullptr);
 // bytes of the bf16 block workspace region holding the O-GEMM A operand
 // (acat, [Nv][3D] bf16), reused by the extension as the FFN hidden when Dff <= 3D
 size_t bf16_workspace_acat_offset(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H);

@@ -388,8 +388,25 @@ __global__ void pack_o_kernel(const float* __restrict__ raw, T* __restrict__ wo,
   }
 }
 
+// Wo^T for the head-slot layout of the O-GEMM A operand (acat [Nv][3][H][S],
+// AttnTcParams.head_slot = S): [D][3*H*S] bf16, zero for the slot padding.
+__global__ void pack_o_slot_kernel(const float* __restrict__ raw, __nv_bfloat16* __restrict__ wo, int D, int H,
+                                   int S) {
+  const int dh = D / H;
+  const int64_t K = 3 * (int64_t)H * S;
+  const int64_t total = (int64_t)D * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = e / K, kk = e % K;
+    const int b = (int)(kk / ((int64_t)H * S));
+    const int r = (int)(kk % ((int64_t)H * S));
+    const int h = r / S, d = r % S;
+    wo[e] = __float2bfloat16_rn(d < dh ? raw_w(raw, b, 3, D)[(int64_t)(h * dh + d) * D + n] : 0.f);
+  }
+}
+
 int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int H, bool bf16,
-                cudaStream_t st, void* wqkv_c, float* bias_c) {
+                cudaStream_t st, void* wqkv_c, float* bias_c, void* wo_s) {
   const int blocks = 148 * 8;
   const QkvPad q = qkv_pad_layout(D, H);
   const int64_t N = bf16 ? q.Npad : 9 * (int64_t)D;
@@ -402,6 +419,8 @@ int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int 
       pack_qkv_kernel<__nv_bfloat16, true><<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wqkv_c, D, H, qc.Npad, qc);
       pack_bias_kernel<<<(unsigned)cdiv(qc.Npad, 128), 128, 0, st>>>(raw, bias_c, D, H, qc.Npad, true, qc);
     }
+    if (wo_s && qkv_compact_ok(D, H))
+      pack_o_slot_kernel<<<blocks, 256, 0, st>>>(raw, (__nv_bfloat16*)wo_s, D, H, qkv_pad_layout(D, H).DP);
   } else {
     pack_qkv_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wqkv, D, H, N, q);
     pack_o_kernel<float, false><<<blocks, 256, 0, st>>>(raw, (float*)wo, D);

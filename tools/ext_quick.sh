@@ -1,2 +1,13 @@
 cd $GRAFT_REPO_ROOT
-for c in 1 3 4 5; do S=10; [ $c = 3 ] && S=3; timeout -s KILL 600 python bench.py --config $c --steps $S --warmup 3 > gpurun_out/r1h_cfg$c.log 2>&1; echo "rc=$?" >> gpurun_out/r1h_cfg$c.log; done
+timeout -s KILL 900 python -m pytest tests -m gpu -x -q > gpurun_out/s_tests.log 2>&1; echo "rc=$?" >> gpurun_out/s_tests.log
+for i in 1 2 3; do
+for lib in tools/_bin/lib_prev.so paper_2501_08453_b200/libvchitect_b200.so; do
+VC_LIB_PATH=$PWD/$lib timeout -s KILL 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/s_b.log 2>&1
+python - $lib <<'PY'
+import json,sys
+for l in open("gpurun_out/s_b.log"):
+    if l.startswith("{"):
+        d=json.loads(l); s=d["block"]["stage_ms"]
+        print(sys.argv[1][-22:], "ms %.3f"%d["ms_per_step"], "sp %.4f tm %.4f fs %.4f o %.4f"%(s["attn_spatial"], s["attn_temporal"], s["attn_fullseq"], s["oproj_gemm"]), "sum %.3f"%sum(s.values()))
+PY
+done; done
