@@ -193,8 +193,44 @@ __global__ void __launch_bounds__(kWarps * 32)
   // the zeros oacc holds there: V's padding is zero-filled in smem)
   __nv_bfloat16* o0 = o + ((int64_t)fr0 * Lv + l) * ldo + (int64_t)h * hs;
   __nv_bfloat16* o1 = o + ((int64_t)fr1 * Lv + l) * ldo + (int64_t)h * hs;
+  int j0 = 0;
+  if (hs == 8 * NT) {
+    // full-width head slot (16-byte aligned rows): a 4x4 word transpose inside
+    // each quad gives thread t the 8 columns of n-tile 4*jg + t, stored as one
+    // 16-byte vector per row instead of four 4-byte ones
+    const int lb = lane & ~3;
+#pragma unroll
+    for (int jg = 0; jg + 4 <= NT; jg += 4) {
+      uint32_t a[4], b[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a[k] = ptx::bf16x2(oacc[jg + k][0] * i0, oacc[jg + k][1] * i0);
+        b[k] = ptx::bf16x2(oacc[jg + k][2] * i1, oacc[jg + k][3] * i1);
+      }
+      uint32_t oa[4] = {0u, 0u, 0u, 0u}, ob[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int want = (t + r) & 3;  // the n-tile whose words this lane hands to lane (t + r) & 3
+        const uint32_t sa = want == 0 ? a[0] : want == 1 ? a[1] : want == 2 ? a[2] : a[3];
+        const uint32_t sb = want == 0 ? b[0] : want == 1 ? b[1] : want == 2 ? b[2] : b[3];
+        const int src = lb | ((t - r) & 3);
+        const uint32_t ra = __shfl_sync(0xffffffffu, sa, src), rb = __shfl_sync(0xffffffffu, sb, src);
+        const int pos = (t - r) & 3;  // the source lane's column pair inside n-tile jg + t
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          oa[q] = pos == q ? ra : oa[q];
+          ob[q] = pos == q ? rb : ob[q];
+        }
+      }
+      const int c = 8 * (jg + t);
+      if (fr0 < F) *reinterpret_cast<uint4*>(o0 + c) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+      if (fr1 < F) *reinterpret_cast<uint4*>(o1 + c) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+    }
+    j0 = NT / 4 * 4;
+  }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
+    if (j < j0) continue;
     const int c = 8 * j + 2 * t;
     if (c < hs) {
       if (fr0 < F) *reinterpret_cast<__nv_bfloat162*>(o0 + c) = __floats2bfloat162_rn(oacc[j][0] * i0, oacc[j][1] * i0);

@@ -8,6 +8,6 @@ import json,sys
 for l in open("gpurun_out/s_b.log"):
     if l.startswith("{"):
         d=json.loads(l); s=d["block"]["stage_ms"]
-        print(sys.argv[1][-22:], "ms %.3f"%d["ms_per_step"], "sp %.4f tm %.4f fs %.4f o %.4f"%(s["attn_spatial"], s["attn_temporal"], s["attn_fullseq"], s["oproj_gemm"]), "sum %.3f"%sum(s.values()))
+        print(sys.argv[1][-22:], "ms %.3f"%d["ms_per_step"], "tm %.4f"%s["attn_temporal"], "sum %.3f"%sum(s.values()))
 PY
 done; done
