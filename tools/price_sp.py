@@ -15,11 +15,11 @@ SHAPES = {2: (16, 1350, 256, 1584, 24, "profiles/r01/bench_config2.json"),
 out = {"what": "PRICED (alpha-beta model on measured single-GPU stage times), not measured: "
                "paper_2501_08453_b200/pricing.py; spec = B200Spec (NVLink 900 GB/s nominal, alpha 10 us assumed)",
        "spec": pricing.B200Spec().as_cluster_kwargs(), "configs": {}}
-# the SP path's layout passes, measured on config 2: SP at P = 1 (5.63 ms,
-# bench.py --sp under torchrun) minus the plain block (5.26 ms) minus the
+# the SP path's layout passes, measured on config 2 (run r1i): SP at P = 1 (5.59 ms,
+# bench.py --sp under torchrun) minus the plain block (4.93 ms) minus the
 # world-1 NCCL all-to-all copy of 635 MB (~0.2 ms at HBM speed); scaled to the
 # other configs by activation size (memory-bound unpacks)
-SP_OVERHEAD_CFG2 = 5.63 - 5.26 - 0.20
+SP_OVERHEAD_CFG2 = 5.59 - 4.93 - 0.20
 for cfg, (F, Lv, Lt, D, H, path) in SHAPES.items():
     stages = json.load(open(os.path.join(ROOT, path)))["block"]["stage_ms"]
     ovh = SP_OVERHEAD_CFG2 * (F * Lv * D) / (16 * 1350 * 1584)
