@@ -129,7 +129,8 @@ __device__ __forceinline__ __nv_bfloat16* out_row(const AttnTcParams& p, int qi,
   while (r + 1 < p.spo.P && p.spo.vb[r + 1] <= lpos) ++r;
   const int vc = p.spo.vb[r + 1] - p.spo.vb[r];
   // base[r] already points at this branch's block for rank r
-  return p.out + p.spo.base[r] + ((int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg + (int64_t)h * p.dh;
+  return p.out + p.spo.base[r] + ((int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg +
+         (int64_t)h * (p.head_slot ? p.head_slot : p.dh);
 }
 
 template <int DP, int C0 = 0, int C1 = DP / 16>

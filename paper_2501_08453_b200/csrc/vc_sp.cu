@@ -35,6 +35,10 @@ inline size_t aup(size_t v) { return (v + 1023) / 1024 * 1024; }
 
 struct Sp {
   int64_t F, Lv, Lt, D, H, dh, Nv, P, rank, Hg, Dg, DP, Lv_ld, Lk_ld;
+  // head-parallel, dh 66: attention outputs in 80-column head slots (S = DP)
+  // through send2 / recv2 and acat [m][3][H][S] (whole-sector stores, the
+  // single-GPU block's layout); BW = acat columns per branch (H*S or D)
+  int64_t S, BW;
   int32_t vb[17];
   int64_t M[16];       // local rows F*vc_r per rank
   // exchange buffers are branch-major: [b'][peer][...]; offsets of the
@@ -67,9 +71,11 @@ int sp_make(const vc_sp_plan* pl, Sp* o, bool gather = false) {
   x.F = s.frames; x.Lv = s.visual_len; x.Lt = s.text_len; x.D = s.dim; x.H = s.heads;
   x.dh = x.D / x.H; x.Nv = x.F * x.Lv; x.P = P; x.rank = pl->rank;
   x.Hg = gather ? x.H : x.H / P;
-  x.Dg = x.Hg * x.dh;
   x.pad = qkv_pad_layout(x.D, x.H);
   x.DP = x.pad.DP;
+  x.S = (!gather && qkv_compact_ok(x.D, x.H)) ? x.DP : 0;
+  x.Dg = x.Hg * (x.S ? x.S : x.dh);
+  x.BW = x.S ? x.H * x.S : x.D;
   x.Lv_ld = round_up(x.Lv, 8);
   x.Lk_ld = round_up(x.Lt + x.Nv, 8);
   for (int r = 0; r <= P; ++r) x.vb[r] = (int32_t)((int64_t)r * x.Lv / P);  // contiguous_bounds
@@ -100,7 +106,7 @@ SpWs sp_ws(const Sp& x) {
   w.qfs = o; o = aup(o + (size_t)x.Nv * qk);
   w.kfs = o; o = aup(o + (size_t)(x.Lt + x.Nv) * qk);
   w.vtfs = o; o = aup(o + (size_t)x.Hg * x.DP * x.Lk_ld * 2);
-  w.acat = o; o = aup(o + (size_t)Mr * 3 * x.D * 2);
+  w.acat = o; o = aup(o + (size_t)Mr * 3 * x.BW * 2);
   w.total = o;
   return w;
 }
@@ -108,13 +114,15 @@ SpWs sp_ws(const Sp& x) {
 struct PackedPtrs {
   const __nv_bfloat16* wqkv;
   const float* bias;
-  const __nv_bfloat16* wo;
+  const __nv_bfloat16* wo;    // [D][3D]
+  const __nv_bfloat16* wo_s;  // [D][3*H*S] head-slot Wo (== wo when the shape has none)
 };
 PackedPtrs packed_ptrs(const Sp& x, const void* packed) {
-  size_t wqkv, bias, wo, total;
-  packed_offsets(x.D, x.H, true, &wqkv, &bias, &wo, &total);
+  size_t wqkv, bias, wo, total, wqkv_c, bias_c, wo_s;
+  packed_offsets(x.D, x.H, true, &wqkv, &bias, &wo, &total, &wqkv_c, &bias_c, &wo_s);
   const char* p = (const char*)packed;
-  return PackedPtrs{(const __nv_bfloat16*)(p + wqkv), (const float*)(p + bias), (const __nv_bfloat16*)(p + wo)};
+  return PackedPtrs{(const __nv_bfloat16*)(p + wqkv), (const float*)(p + bias), (const __nv_bfloat16*)(p + wo),
+                    (const __nv_bfloat16*)(p + wo_s)};
 }
 
 struct UnpackArgs {
@@ -203,12 +211,13 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
   }
 }
 
-// recv2[b'][g][m][Dg] -> acat[m][b'*2D + g*Dg + c]  (b'=0 spatial cols [0,D), b'=1 full-seq [2D,3D))
+// recv2[b'][g][m][Dg] -> acat[m][b'*2BW + g*Dg + c]  (b'=0 spatial cols [0,BW), b'=1 full-seq [2BW,3BW);
+// BW = D, or H*S with head slots)
 // One warp per (b', g, m) row, lanes across the row: 16-byte words when Dg and
 // D are multiples of 8 (every row then starts 16-byte aligned), else 4-byte.
 __global__ void __launch_bounds__(256) sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv,
                                                          __nv_bfloat16* __restrict__ acat, int P, int64_t Mr,
-                                                         int64_t Dg, int64_t D) {
+                                                         int64_t Dg, int64_t D) {  // D: branch width BW
   const int lane = threadIdx.x & 31;
   const int64_t rows = (int64_t)P * 2 * Mr;
   const bool v16 = (Dg % 8) == 0 && (D % 8) == 0;
@@ -401,7 +410,8 @@ int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loca
     VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
     profile_mark(st, "sp_qkv_gemm");
     // temporal branch is rank-local: sequence = local position, tokens = frames (stride vc)
-    VC_TRY(launch_temporal_mma(tm, 3 * x.D, x.D, acat + x.D, 3 * x.D, (int)x.F, vc, (int)x.H, (int)x.dh, st));
+    VC_TRY(launch_temporal_mma(tm, 3 * x.D, x.D, acat + x.BW, 3 * x.BW, (int)x.F, vc, (int)x.H, (int)x.dh, st,
+                               (int)x.S));
     profile_mark(st, "sp_attn_temporal");
   }
   return VC_OK;
@@ -456,6 +466,7 @@ int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed, const void* 
   a.H = (int)x.Hg; a.dh = (int)x.dh; a.scale_log2 = scale_log2;
   a.out = (bf*)send2; a.ld_out = 0; a.col_off = 0; a.out_seq_rows = 0;
   a.spo.P = (int)x.P; a.spo.branch = branch; a.spo.F = (int)x.F; a.spo.Lv = (int)x.Lv; a.spo.Dg = x.Dg;
+  a.head_slot = (int)x.S;
   for (int r = 0; r <= x.P; ++r) { a.spo.vb[r] = x.vb[r]; a.spo.base[r] = branch * x.half2 + x.s2_off[r]; }
   if (branch == 0) {
     a.Lq = (int)x.Lv; a.Lk = (int)x.Lv; a.n_bias = 0; a.bias_log2 = 0.f;
@@ -490,14 +501,14 @@ int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, 
   {
     const int64_t rows = x.P * 2 * Mr;  // one warp per row
     const int blocks = (int)std::min<int64_t>(cdiv(rows, 8), 148 * 16);
-    sp_unpack2_kernel<<<blocks, 256, 0, st>>>((const bf*)recv2, acat, (int)x.P, Mr, x.Dg, x.D);
+    sp_unpack2_kernel<<<blocks, 256, 0, st>>>((const bf*)recv2, acat, (int)x.P, Mr, x.Dg, x.BW);
     VC_CHECK_LAUNCH();
     profile_mark(st, "sp_unpack2");
   }
   GemmTcParams g{};
-  g.M = Mr; g.N = (int)x.D; g.K = (int)(3 * x.D);
+  g.M = Mr; g.N = (int)x.D; g.K = (int)(3 * x.BW);
   g.out_f32 = out_local; g.ldo = x.D; g.R = add_residual ? x_local : nullptr; g.ldr = x.D;
-  VC_TRY(launch_gemm_tc(acat, 3 * x.D, pp.wo, 3 * x.D, g, EPI_F32, st));
+  VC_TRY(launch_gemm_tc(acat, 3 * x.BW, x.S ? pp.wo_s : pp.wo, 3 * x.BW, g, EPI_F32, st));
   profile_mark(st, "sp_oproj_gemm");
   return VC_OK;
 }

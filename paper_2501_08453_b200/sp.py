@@ -79,12 +79,15 @@ def check_plan(frames, visual_len, heads, p):
 def exchange_counts(frames, visual_len, heads, dim, p, rank, head_pad):
     """Per-peer element counts of the two all-to-alls (bf16 elements):
     send1/recv1 carry q,k,v of 2 branches for H/P heads (head dim padded to
-    head_pad); send2/recv2 carry 2 branches' attention outputs (H/P * dh).
+    head_pad); send2/recv2 carry 2 branches' attention outputs (H/P * dh, or
+    H/P head_pad-wide head slots when dh is 66).
     The buffers are branch-major (vc_sp.cu): each branch is one half, split by
     peer with half these counts (branch_counts)."""
     vb = contiguous_bounds(visual_len, p)
     M = [frames * (vb[r + 1] - vb[r]) for r in range(p)]
-    hg, dg = heads // p, dim // p
+    # dh 66 (the 2B shape): outputs travel in head_pad-wide head slots (vc_sp.cu Sp.S)
+    hg = heads // p
+    dg = hg * (head_pad if dim // heads == 66 else dim // heads)
     return {
         "send1": [6 * M[rank] * hg * head_pad for _ in range(p)],
         "recv1": [6 * M[r] * hg * head_pad for r in range(p)],

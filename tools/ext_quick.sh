@@ -1,13 +1,17 @@
 cd $GRAFT_REPO_ROOT
-timeout -s KILL 900 python -m pytest tests -m gpu -x -q > gpurun_out/s_tests.log 2>&1; echo "rc=$?" >> gpurun_out/s_tests.log
-for i in 1 2 3; do
-for lib in tools/_bin/lib_prev.so paper_2501_08453_b200/libvchitect_b200.so; do
-VC_LIB_PATH=$PWD/$lib timeout -s KILL 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/s_b.log 2>&1
-python - $lib <<'PY'
-import json,sys
-for l in open("gpurun_out/s_b.log"):
-    if l.startswith("{"):
-        d=json.loads(l); s=d["block"]["stage_ms"]
-        print(sys.argv[1][-22:], "ms %.3f"%d["ms_per_step"], "tm %.4f"%s["attn_temporal"], "sum %.3f"%sum(s.values()))
-PY
-done; done
+timeout -s KILL 900 python -m pytest tests -m gpu -x -q > gpurun_out/sps_tests.log 2>&1; echo "rc=$?" >> gpurun_out/sps_tests.log
+export RANK=0 WORLD_SIZE=1 LOCAL_RANK=0 MASTER_ADDR=127.0.0.1 MASTER_PORT=29655
+for i in 1 2; do
+timeout -s KILL 300 python bench.py --sp --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/sp1_plain.log 2>&1
+python -c "
+import json
+for l in open('gpurun_out/sp1_plain.log'):
+    if l.startswith('{'): d=json.loads(l); print('sp1', d['value'], d['ms_per_step'], d['a2a'])
+"
+timeout -s KILL 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/pl.log 2>&1
+python -c "
+import json
+for l in open('gpurun_out/pl.log'):
+    if l.startswith('{'): d=json.loads(l); print('plain', d['value'], d['ms_per_step'])
+"
+done
