@@ -224,7 +224,9 @@ VC_API int vc_sp_check(const vc_sp_plan* plan);
 VC_API int vc_sp_bounds(const vc_sp_plan* plan, int32_t* vbounds);
 VC_API size_t vc_sp_workspace_bytes(const vc_sp_plan* plan);
 /* which: 0 send1 to peer, 1 recv1 from peer, 2 send2 to peer, 3 recv2 from
- * peer. -1 on error. */
+ * peer (bf16 elements as laid out: head dim padded to DP, dh-66 outputs in
+ * DP-wide head slots); 4..7 the same without that padding (the reference's
+ * payload, executor.py:344-347, :395-412). -1 on error. */
 VC_API int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which,
                                     int32_t peer);
 /* x_local [F][vc_r][D] fp32, prompt [Lt][D] fp32 -> send1 (bf16). */

@@ -2,6 +2,8 @@
 
     python -m paper_2501_08453_b200.build            # incremental
     python -m paper_2501_08453_b200.build --force
+    python -m paper_2501_08453_b200.build --force --tuning   # A/B switches read
+                                                             # from the environment (vc_tuning.h)
 
 nvcc compiles every csrc/*.cu with -gencode arch=compute_100a,code=sm_100a
 -lineinfo -O3 and links one shared library next to this file (git-ignored,
@@ -73,4 +75,5 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True,
-          extra=["-Xptxas", "-v"] if "--ptxas-v" in sys.argv else [])
+          extra=(["-Xptxas", "-v"] if "--ptxas-v" in sys.argv else [])
+          + (["-DVC_TUNING"] if "--tuning" in sys.argv else []))

@@ -24,17 +24,14 @@
 //         K-major, double buffered) for the SS MMA.
 #include <math.h>
 
-#include "vc_attn_tc.h"
-#include "vc_gemm_tc.h"
-#include "vc_ptx.cuh"
+#include "vc_attn_tc_common.cuh"
 
 namespace vc {
 
 namespace {
 
-constexpr int BQ = 128, BKV = 128;
+using namespace attn;  // BQ, BKV, kRescaleThreshold, qk_desc, store_out (vc_attn_tc_common.cuh)
 constexpr int kThreads = 256;
-constexpr float kRescaleThreshold = 8.0f;
 
 template <int DP>
 struct Cfg {
@@ -54,19 +51,6 @@ struct Cfg {
   static constexpr int KSTEPS = DP / 16;               // MMA K steps of S = Q K^T
   static_assert(SMEM <= 232448, "shared memory budget");
 };
-
-// Byte offset, inside a Q/K tile, of the head-dim 16-chunk c; tiles are laid
-// out as N64 SW128 sub-tiles [128 rows][128 B] followed by the SW32 tail
-// [128 rows][32 B].
-template <int DP>
-__device__ __forceinline__ uint64_t qk_desc(uint32_t tile_addr, int c) {
-  constexpr int N64 = Cfg<DP>::N64;
-  if (c < 4 * N64) {
-    const uint32_t a = tile_addr + (c >> 2) * (BQ * 128) + (c & 3) * 32;
-    return ptx::smem_desc(a, 0, 1024, ptx::kLayoutSW128);
-  }
-  return ptx::smem_desc(tile_addr + N64 * (BQ * 128), 0, 256, ptx::kLayoutSW32);
-}
 
 template <int DP>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -300,43 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- epilogue: O / l -> bf16 -> out[row][col_off + h*dh + d], d < dh ----
     ptx::mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     ptx::fence_after_sync();
-    const int qi = q0 + row;
-    const float inv = 1.f / l;
-    __nv_bfloat16* orow = nullptr;
-    if (qi < p.Lq) {
-      if (p.spo.P == 0) {
-        orow = p.out + (int64_t)(seq * p.out_seq_rows + qi) * p.ld_out + p.col_off + (int64_t)h * p.dh;
-      } else {  // sequence-parallel: straight into the all-to-all #2 send buffer
-        const int f = p.spo.branch == 0 ? seq : qi / p.spo.Lv;
-        const int lpos = p.spo.branch == 0 ? qi : qi - f * p.spo.Lv;
-        int r = 0;
-        while (r + 1 < p.spo.P && p.spo.vb[r + 1] <= lpos) ++r;
-        const int vc = p.spo.vb[r + 1] - p.spo.vb[r];
-        const int64_t Mr = (int64_t)p.spo.F * vc;
-        orow = p.out + p.spo.base[r] + (p.spo.branch * Mr + (int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg +
-               (int64_t)h * p.dh;
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < DP / 16; ++c) {
-      uint32_t r[16];
-      ptx::tmem_ld16(tO + lane_off + c * 16, r);
-      ptx::tmem_ld_wait();
-      if (orow) {
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const int d = c * 16 + i;
-          if (d + 1 < p.dh) {
-            __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv);
-            if (((p.col_off + h * p.dh + d) & 1) == 0)
-              *reinterpret_cast<__nv_bfloat162*>(orow + d) = b;
-            else { orow[d] = b.x; orow[d + 1] = b.y; }
-          } else if (d < p.dh) {
-            orow[d] = __float2bfloat16_rn(__uint_as_float(r[i]) * inv);
-          }
-        }
-      }
-    }
+    // shared epilogue: plain rows, head slots or the SP send layout (out_row)
+    store_out<DP>(p, tO + lane_off, l, q0 + row, seq, h);
   }
   ptx::fence_before_sync();
   __syncthreads();
@@ -400,29 +349,13 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
   if (p.Lq <= 0 || nseq <= 0) return VC_OK;
   if (p.Lk <= 0) { set_error("attention needs at least one key"); return VC_EINVAL; }
   if (nseq > 65535 || p.H > 65535) { set_error("attention grid too large"); return VC_ENOTSUP; }
-  // A/B switch for profiling (VC_ATTN_IMPL): 1 one query tile per CTA, 2 one
-  // softmax thread per row, else (default) attn_tc3.  Slower variants measured
-  // in round 1 (Q/P in TMEM, 64-key double-buffered S, four warps per row,
-  // CTA pairs; persistent) are in git history at 20e1484 and 028589b;
-  // profiles/r01/attn_study/README.md.
-  static const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 3;
-  // persistent tc3 (VC_ATTN_PERSIST, A/B switch): 0 (default) never, 1 short
-  // key ranges (<= 4096 keys: the spatial branch), 2 always.  Correct on every
-  // test shape, but measured 0.401-0.405 vs 0.396-0.399 ms on the spatial
-  // branch (profiles/r01/attn_study/README.md), so off.
-  static const int persist = getenv("VC_ATTN_PERSIST") ? atoi(getenv("VC_ATTN_PERSIST")) : 0;
-  const bool use_p = impl == 3 && (persist == 2 || (persist == 1 && p.Lk <= 4096)) && p.spo.P == 0;
-  if (use_p && DP == 64) return launch_attn_tc3p<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-  if (use_p && DP == 80) return launch_attn_tc3p<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+  // DP <= 80 (the 2B head dim 66 -> 80, dh 64): the two-tile split-row
+  // kernel (vc_attn_tc3.cu); DP = 128: the one-tile kernel above.  Variants
+  // measured slower in round 1 are in git history
+  // (profiles/r01/attn_study/README.md).
   switch (DP) {
-    case 64:
-      if (impl == 1) return launch_dp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      if (impl == 2) return launch_attn_tc2<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-    case 80:
-      if (impl == 1) return launch_dp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      if (impl == 2) return launch_attn_tc2<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-      return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 64: return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 80: return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 128: return launch_dp<128>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
   }
   set_error("tcgen05 attention: unsupported padded head dim %d", DP);

@@ -35,20 +35,10 @@ struct AttnTcParams {
   int32_t head_slot;
 };
 
-// Two-query-tile (ping-pong) kernel for DP <= 80 (vc_attn_tc2.cu).
-template <int DP>
-int launch_attn_tc2(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
-
 // Split-row variant: each tile's softmax on two warpgroups (vc_attn_tc3.cu).
 template <int DP>
 int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
                     int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
-
-// Persistent variant of launch_attn_tc3 (one CTA per SM walking the work items).
-template <int DP>
-int launch_attn_tc3p(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                     int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
 
 // Padded head dim the tensor-core kernel uses for dh (0: unsupported).
 int attn_tc_head_pad(int dh);

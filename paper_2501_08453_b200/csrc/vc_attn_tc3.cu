@@ -1,8 +1,9 @@
 // Flash attention, two query tiles per CTA ping-ponging on one tensor core,
 // each tile's softmax split across TWO warpgroups ("split rows").
 //
-// Same semantics, layouts and MMA schedule as vc_attn_tc2.cu (DP <= 80: the
-// 2B shape dh 66 -> 80).  What changes is the softmax: in vc_attn_tc2 one
+// Same semantics and layouts as vc_attn_tc.cu (DP <= 80: the 2B shape dh
+// 66 -> 80), two query tiles per CTA.  What changes is the softmax: in the
+// round-1 two-tile kernel with one softmax thread per row (git history) one
 // thread owns a query row's 128 logits of a key tile, and the measured
 // per-tile chain (TMEM load -> row max -> TMEM reload -> 128 exp2 -> P store,
 // tools/attn_trace.cu) ran at ~0.3 instructions/clock per warp, so two
@@ -17,6 +18,7 @@
 // 18 warps: w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w17 softmax
 // (w = 2 + 8*tile + 4*half + i; w % 4 is the TMEM lane quarter).
 #include "vc_attn_tc_common.cuh"
+#include "vc_tuning.h"
 
 namespace vc {
 
@@ -400,343 +402,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
         l += __uint_as_float(other);
       }
       VC_TR3(trs, 1 + sw, 255, 2);  // row sum read
-#ifdef VC_ATTN_STAGED_OUT
-      {  // rows staged in this tile's K stage (free once the tile's last P.V is done), copied out a warp per row
-        const int sdh = (p.dh + 1) & ~1;
-        __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + CF::OFF_K + t * CF::QK_BYTES);
-        if (half == 0) stage_out<DP, 0, CF::NC0>(tO, l, stg + row * sdh, p.dh);
-        else stage_out<DP, CF::NC0, CF::NC>(tO, l, stg + row * sdh, p.dh);
-        ptx::named_bar_sync(9 + t, 256);
-        copy_out_rows(p, stg, sdh, q0 + t * BQ, BQ, seq, h, sw & 7, 8, lane);
-      }
-#else
       if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
       else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
-#endif
       VC_TR3(trs, 1 + sw, 255, 1);  // output stored
     }
   }
   ptx::fence_before_sync();
   __syncthreads();
   VC_TR3(tr && threadIdx.x == 32, 0, 255, 4);  // all warps done
-  if (warp == 1) {
-    ptx::fence_after_sync();
-    ptx::tmem_dealloc(tmem, 512);
-  }
-}
-
-// ---- persistent variant (short sequences) ----------------------------------
-// Same roles, schedule and softmax as attn_tc3_kernel (P half in TMEM, Q in
-// smem, ones column, lock-step issue), but each CTA walks work items
-// (query-block pair, head, sequence) = blockIdx.x, +gridDim.x, ...  What that
-// buys for short sequences (the 1350-token spatial branch: 11 key blocks per
-// item): the next item's Q and K/V stream in while the current item's last
-// blocks run, its first S MMAs overlap the current item's output epilogue,
-// and the output stores drain under the next item instead of holding the SM
-// at EXIT (ncu: 15% of the spatial kernel's warp samples).  Barrier phases run
-// on per-role block counters across items; two new barriers: q_empty (the
-// item's last S MMAs have read Q) and o_free[t] (the softmax warps have read
-// tile t's O, so the next item's first P.V may overwrite it).
-template <int DP, int POLY, bool ONES>
-__global__ void __launch_bounds__(kThreads3, 1)
-    attn_tc3p_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
-                     const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
-                     const __grid_constant__ CUtensorMap tmV, const AttnTcParams p, const int qblocks,
-                     const int n_items) {
-  using CF = Cfg3<DP>;
-  constexpr int KS = CF::KS;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;      // [KS]
-  uint64_t* k_empty = k_full + KS;  // [KS]
-  uint64_t* v_full = k_empty + KS;  // [KS]
-  uint64_t* v_empty = v_full + KS;  // [KS]
-  uint64_t* s_full = v_empty + KS;  // [2 tiles]
-  uint64_t* s_empty = s_full + 2;   // [2 tiles]
-  uint64_t* p_full = s_empty + 2;   // [2 tiles]
-  uint64_t* pv_done = p_full + 2;   // [2 tiles]
-  uint64_t* q_empty = pv_done + 2;  // the item's S MMAs are done with Q
-  uint64_t* o_free = q_empty + 1;   // [2 tiles] O read out by the softmax warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
-
-  const int warp = threadIdx.x >> 5;
-  const int n_tiles = (p.Lk + BKV - 1) / BKV;
-  auto decode = [&](int item, int& q0, int& h, int& seq) {
-    const int qb = item % qblocks;
-    const int rest = item / qblocks;
-    h = rest % p.H;
-    seq = rest / p.H;
-    q0 = qb * (2 * BQ);
-  };
-
-  if (warp == 0 && ptx::elect_one()) {
-    ptx::prefetch_tmap(&tmQ64); ptx::prefetch_tmap(&tmK64); ptx::prefetch_tmap(&tmV);
-    if (CF::TAIL) { ptx::prefetch_tmap(&tmQ16); ptx::prefetch_tmap(&tmK16); }
-    ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(q_empty, 1);
-    for (int i = 0; i < KS; ++i) {
-      ptx::mbar_init(&k_full[i], 1);
-      ptx::mbar_init(&k_empty[i], 1);
-      ptx::mbar_init(&v_full[i], 1);
-      ptx::mbar_init(&v_empty[i], 1);
-    }
-    for (int t = 0; t < 2; ++t) {
-      ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&s_empty[t], 256);
-      ptx::mbar_init(&p_full[t], 256);
-      ptx::mbar_init(&pv_done[t], 1);
-      ptx::mbar_init(&o_free[t], 256);
-    }
-    ptx::fence_barrier_init();
-  }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
-  ptx::fence_before_sync();
-  __syncthreads();
-  ptx::fence_after_sync();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (ptx::elect_one()) {
-      int g = 0, it = 0;  // g: key blocks loaded so far (stage ring position)
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        int q0, h, seq;
-        decode(item, q0, h, seq);
-        if (it > 0) ptx::mbar_wait(q_empty, (it - 1) & 1);  // previous item's S MMAs read Q
-        ptx::mbar_arrive_expect_tx(q_full, 2 * CF::QK_BYTES);
-        for (int t = 0; t < 2; ++t) {
-          uint8_t* sQ = smem + CF::OFF_Q + t * CF::QK_BYTES;
-          for (int c = 0; c < CF::N64; ++c)
-            ptx::tma_load_4d(sQ + c * BQ * 128, &tmQ64, q_full, c * 64, h, q0 + t * BQ, seq);
-          if (CF::TAIL) ptx::tma_load_4d(sQ + CF::N64 * BQ * 128, &tmQ16, q_full, CF::N64 * 64, h, q0 + t * BQ, seq);
-        }
-        for (int j = 0; j < n_tiles; ++j, ++g) {
-          const int s = g % KS;
-          const uint32_t ph = ((g / KS) & 1) ^ 1;
-          const int k0 = j * BKV;
-          ptx::mbar_wait(&k_empty[s], ph);
-          ptx::mbar_arrive_expect_tx(&k_full[s], CF::QK_BYTES);
-          uint8_t* sK = smem + CF::OFF_K + s * CF::QK_BYTES;
-          for (int c = 0; c < CF::N64; ++c)
-            ptx::tma_load_4d(sK + c * BKV * 128, &tmK64, &k_full[s], c * 64, h, k0, seq);
-          if (CF::TAIL) ptx::tma_load_4d(sK + CF::N64 * BKV * 128, &tmK16, &k_full[s], CF::N64 * 64, h, k0, seq);
-          ptx::mbar_wait(&v_empty[s], ph);
-          ptx::mbar_arrive_expect_tx(&v_full[s], CF::V_BYTES);
-          uint8_t* sV = smem + CF::OFF_V + s * CF::V_BYTES;
-          ptx::tma_load_4d(sV, &tmV, &v_full[s], k0, 0, h, seq);
-          ptx::tma_load_4d(sV + DP * 128, &tmV, &v_full[s], k0 + 64, 0, h, seq);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKV);
-    constexpr uint32_t idO = ptx::idesc_bf16_f32(BQ, DP);
-    int g = 0, it = 0;               // key blocks consumed; items
-    int ns[2] = {0, 0}, np[2] = {0, 0}, ni[2] = {0, 0};  // per tile: S issued, P.V issued, items
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      int q0, h, seq;
-      decode(item, q0, h, seq);
-      const int ntile = q0 + BQ < p.Lq ? 2 : 1;
-      ptx::mbar_wait(q_full, it & 1);
-      // last: the item's final S block -> after the last tile's MMAs, release
-      // Q (commit from the issuing thread: it tracks that thread's MMAs)
-      auto issue_s = [&](int t, int gb, bool last) {  // gb: global key block (stage)
-        const int ks = gb % KS;
-        if (ns[t] > 0) ptx::mbar_wait(&s_empty[t], (ns[t] - 1) & 1);
-        ptx::fence_after_sync();
-        if (ptx::elect_one()) {
-          const uint32_t aQ = ptx::smem_u32(smem + CF::OFF_Q + t * CF::QK_BYTES);
-          const uint32_t aK = ptx::smem_u32(smem + CF::OFF_K + ks * CF::QK_BYTES);
-#pragma unroll
-          for (int c = 0; c < CF::KSTEPS; ++c)
-            ptx::mma_bf16_ss(tmem + t * 256, qk_desc<DP>(aQ, c), qk_desc<DP>(aK, c), idS, c > 0);
-          ptx::mma_commit(&s_full[t]);
-          if (t == ntile - 1) {
-            ptx::mma_commit(&k_empty[ks]);
-            if (last) ptx::mma_commit(q_empty);
-          }
-        }
-        __syncwarp();
-        ++ns[t];
-      };
-      auto issue_pv = [&](int t, int j, int gb) {
-        const int ks = gb % KS;
-        ptx::mbar_wait(&p_full[t], np[t] & 1);
-        if (j == 0 && ni[t] > 0) ptx::mbar_wait(&o_free[t], (ni[t] - 1) & 1);  // O of the last item read out
-        ptx::fence_after_sync();
-        if (ptx::elect_one()) {
-          const uint32_t aP = ptx::smem_u32(smem + CF::OFF_P + t * CF::P_BYTES);
-          const uint32_t aV = ptx::smem_u32(smem + CF::OFF_V + ks * CF::V_BYTES);
-#pragma unroll
-          for (int c = 0; c < BKV / 16; ++c) {
-            const uint64_t ad = ptx::smem_desc(aP + (c >> 2) * (BQ * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
-            const uint64_t bd = ptx::smem_desc(aV + (c >> 2) * (DP * 128) + (c & 3) * 32, 0, 1024, ptx::kLayoutSW128);
-            if (c < 4)
-              ptx::mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + CF::QCOL + 8 * c, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
-            else
-              ptx::mma_bf16_ss(tmem + t * 256 + 128, ad, bd, idO, (j > 0 || c > 0) ? 1u : 0u);
-          }
-          ptx::mma_commit(&pv_done[t]);
-          if (t == ntile - 1) ptx::mma_commit(&v_empty[ks]);
-        }
-        __syncwarp();
-        ++np[t];
-      };
-      const int g0 = g;
-      ptx::mbar_wait(&k_full[g0 % KS], (g0 / KS) & 1);
-      issue_s(0, g0, n_tiles == 1);
-      if (ntile == 2) issue_s(1, g0, n_tiles == 1);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int gb = g0 + j;
-        const bool more = j + 1 < n_tiles;
-        if (more) ptx::mbar_wait(&k_full[(gb + 1) % KS], ((gb + 1) / KS) & 1);
-        ptx::mbar_wait(&v_full[gb % KS], (gb / KS) & 1);
-        if (more) issue_s(0, gb + 1, j + 2 == n_tiles);
-        if (more && ntile == 2) issue_s(1, gb + 1, j + 2 == n_tiles);
-        issue_pv(0, j, gb);
-        if (ntile == 2) issue_pv(1, j, gb);
-      }
-      g += n_tiles;
-      ++ni[0];
-      if (ntile == 2) ++ni[1];
-    }
-  } else {
-    // ===================== softmax, correction, epilogue =====================
-    const int sw = warp - 2;
-    const int t = sw >> 3;
-    const int half = (sw >> 2) & 1;
-    const int quarter = warp & 3;
-    const int lane = threadIdx.x & 31;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t tS = tmem + t * 256 + lane_off + half * 64;
-    const uint32_t tO = tmem + t * 256 + 128 + lane_off;
-    const uint32_t tX = tmem + t * 256 + CF::XCOL + lane_off;
-    const uint32_t bar_id = 1 + t * 4 + quarter;
-    const uint32_t rowp = ptx::smem_u32(smem + CF::OFF_P + t * CF::P_BYTES) + half * (BQ * 128) + row * 128;
-    int nb = 0;  // key blocks this tile has processed (barrier phases)
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      int q0, h, seq;
-      decode(item, q0, h, seq);
-      const int ntile = q0 + BQ < p.Lq ? 2 : 1;
-      if (t >= ntile) continue;  // no query rows in this tile for this item
-      float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < n_tiles; ++j, ++nb) {
-        const int kt = j * BKV;
-        const int k0 = kt + half * 64;
-        const bool slow = kt < p.n_bias || kt + BKV > p.Lk;
-        ptx::mbar_wait(&s_full[t], nb & 1);
-        ptx::fence_after_sync();
-        uint32_t r[64];
-        ptx::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(r));
-        ptx::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-        ptx::tmem_ld_wait();
-        ptx::fence_before_sync();
-        ptx::mbar_arrive(&s_empty[t]);
-        if (slow) {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) {
-            float x = __uint_as_float(r[i]) * p.scale_log2;
-            if (k0 + i < p.n_bias) x += p.bias_log2;
-            if (k0 + i >= p.Lk) x = -INFINITY;
-            r[i] = __float_as_uint(x);
-          }
-        }
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int i = 0; i < 64; ++i) m4[i & 3] = fmaxf(m4[i & 3], __uint_as_float(r[i]));
-        float pm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-        if (!slow) pm *= p.scale_log2;
-        float other;
-        {
-          const uint32_t xc = tX + 2 * (nb & 1);
-          ptx::tmem_st1(xc + half, __float_as_uint(pm));
-          ptx::tmem_st_wait();
-          ptx::fence_before_sync();
-          ptx::named_bar_sync(bar_id, 64);
-          ptx::fence_after_sync();
-          uint32_t o;
-          ptx::tmem_ld1(xc + (half ^ 1), o);
-          ptx::tmem_ld_wait();
-          other = __uint_as_float(o);
-        }
-        const float mx = fmaxf(pm, other);
-        float alpha = 1.f;
-        if (mx > m_used + kRescaleThreshold) {
-          alpha = ptx::ex2(m_used - mx);
-          m_used = mx;
-        }
-        if (nb > 0) {  // single P buffer per tile: the previous P.V (this or the last item) is done with it
-          ptx::mbar_wait(&pv_done[t], (nb - 1) & 1);
-          ptx::fence_after_sync();
-        }
-        const float sc = slow ? 1.f : p.scale_log2;
-        const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m_used, -m_used);
-        float2 s2 = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          float2 e = ptx::ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nm2);
-          if (POLY > 0 && ((i >> 1) % (POLY > 0 ? POLY : 1)) == POLY - 1) {
-            e = ptx::ex2_poly2(e);
-          } else {
-            e.x = ptx::ex2(e.x);
-            e.y = ptx::ex2(e.y);
-          }
-          if (!ONES) {
-            if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
-          }
-          pk[i >> 1] = ptx::bf16x2(e.x, e.y);
-        }
-        if (half == 0) {
-          ptx::tmem_st32(tmem + t * 256 + lane_off + CF::QCOL, pk);
-          ptx::tmem_st_wait();
-        } else {
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            ptx::sts128(rowp + ((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
-        if (!ONES) {
-          s2 = ptx::fadd2(s2, s2b);
-          l = l * alpha + (s2.x + s2.y);
-        }
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          if (half == 0) rescale_o<DP, 0, CF::NC0>(tO, alpha);
-          else rescale_o<DP, CF::NC0, CF::NC>(tO, alpha);
-        }
-        ptx::fence_proxy_async_smem();
-        ptx::fence_before_sync();
-        ptx::mbar_arrive(&p_full[t]);
-      }
-      ptx::mbar_wait(&pv_done[t], (nb - 1) & 1);
-      ptx::fence_after_sync();
-      if (ONES) {
-        uint32_t r1;
-        ptx::tmem_ld1(tO + p.dh, r1);
-        ptx::tmem_ld_wait();
-        l = __uint_as_float(r1);
-      } else {
-        ptx::tmem_st1(tX + 4 + half, __float_as_uint(l));
-        ptx::tmem_st_wait();
-        ptx::fence_before_sync();
-        ptx::named_bar_sync(bar_id, 64);
-        ptx::fence_after_sync();
-        uint32_t other;
-        ptx::tmem_ld1(tX + 4 + (half ^ 1), other);
-        ptx::tmem_ld_wait();
-        l += __uint_as_float(other);
-      }
-      if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
-      else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
-      ptx::fence_before_sync();  // TMEM reads of O ordered before the next item's first P.V
-      ptx::mbar_arrive(&o_free[t]);
-    }
-  }
-  ptx::fence_before_sync();
-  __syncthreads();
   if (warp == 1) {
     ptx::fence_after_sync();
     ptx::tmem_dealloc(tmem, 512);
@@ -757,17 +430,16 @@ int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const v
   using CF = Cfg3<DP>;
   AttnMaps m;
   VC_TRY(make_attn_maps<DP>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key));
-  static const int poly = getenv("VC_POLY_EVERY") ? atoi(getenv("VC_POLY_EVERY")) : kPolyEvery3;
-  static const bool no_ones = getenv("VC_NO_ONES_COLUMN") != nullptr;
-  const bool ones = !no_ones && p.dh < DP;
-  // Q in TMEM (default) needs 16-byte aligned Q rows; VC_ATTN_QSMEM=1 keeps Q in smem
-  static const bool q_smem = getenv("VC_ATTN_QSMEM") && atoi(getenv("VC_ATTN_QSMEM")) != 0;
-  // P half in TMEM (default; VC_ATTN_PHALF=0 -> Q in TMEM instead, both do not fit)
-  static const bool ph = !(getenv("VC_ATTN_PHALF") && atoi(getenv("VC_ATTN_PHALF")) == 0);
-  const bool qt = !ph && !q_smem && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+  // defaults: 1 exp pair in 4 on the FMA polynomial, the ones column whenever
+  // dh < DP, P half in TMEM (so Q stays in smem), lock-step MMA issue
+  static const int poly = tuning_int("VC_POLY_EVERY", kPolyEvery3);
+  const bool ones = tuning_int("VC_NO_ONES_COLUMN", 0) == 0 && p.dh < DP;
+  static const bool ph = tuning_int("VC_ATTN_PHALF", 1) != 0;
+  // Q in TMEM (only without the P half; needs 16-byte aligned Q rows)
+  const bool qt = !ph && tuning_int("VC_ATTN_QSMEM", 0) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   // MMA issue order: lock-step (S_A S_B PV_A PV_B, default) or ping-pong (S_A PV_A S_B PV_B)
-  static const bool lock = !(getenv("VC_ATTN_PINGPONG") && atoi(getenv("VC_ATTN_PINGPONG")) != 0);
+  static const bool lock = tuning_int("VC_ATTN_PINGPONG", 0) == 0;
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
 #define VC_ATTN3_CASE(PV, ON, Q, PHV)                                                                      \
   if (poly == PV && ones == ON && qt == Q && ph == PHV) {                                                  \
@@ -782,6 +454,9 @@ int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const v
     VC_CHECK_LAUNCH();                                                                                     \
     return VC_OK;                                                                                          \
   }
+  VC_ATTN3_CASE(4, true, false, true)
+  VC_ATTN3_CASE(4, false, false, true)
+#ifdef VC_TUNING
   VC_ATTN3_CASE(0, false, false, false)
   VC_ATTN3_CASE(0, true, false, false)
   VC_ATTN3_CASE(4, false, false, false)
@@ -794,52 +469,10 @@ int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const v
   VC_ATTN3_CASE(4, true, true, false)
   VC_ATTN3_CASE(2, true, true, false)
   VC_ATTN3_CASE(3, true, true, false)
-  VC_ATTN3_CASE(4, true, false, true)
   VC_ATTN3_CASE(3, true, false, true)
-  VC_ATTN3_CASE(4, false, false, true)
+#endif
 #undef VC_ATTN3_CASE
-  set_error("VC_POLY_EVERY must be 0 or 4 (2, 3 with the ones column)");
-  return VC_EINVAL;
-}
-
-// Persistent launch (attn_tc3p_kernel): one CTA per SM walking the
-// (query-block pair, head, sequence) items; only the default configuration
-// (P half in TMEM, Q in smem, lock-step issue).
-template <int DP>
-int launch_attn_tc3p(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                     int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
-  using CF = Cfg3<DP>;
-  static_assert(CF::OFF_BAR + (1 + 4 * CF::KS + 8 + 3) * 8 + 4 <= CF::SMEM - 1024, "barrier area");
-  AttnMaps m;
-  VC_TRY(make_attn_maps<DP>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key));
-  const bool ones = p.dh < DP;
-  const int qblocks = (int)cdiv(p.Lq, 2 * BQ);
-  const int64_t items = (int64_t)qblocks * p.H * nseq;
-  if (items > INT32_MAX) { set_error("too many attention work items"); return VC_ENOTSUP; }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  const int grid = (int)std::min<int64_t>(items, sms);
-#define VC_ATTN3P_CASE(ON)                                                                                   \
-  if (ones == ON) {                                                                                          \
-    static bool attr = false;                                                                                \
-    if (!attr) {                                                                                             \
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc3p_kernel<DP, 4, ON>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         CF::SMEM));                                                         \
-      attr = true;                                                                                           \
-    }                                                                                                        \
-    attn_tc3p_kernel<DP, 4, ON><<<grid, kThreads3, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p, qblocks, \
-                                                                   (int)items);                              \
-    VC_CHECK_LAUNCH();                                                                                       \
-    return VC_OK;                                                                                            \
-  }
-  VC_ATTN3P_CASE(true)
-  VC_ATTN3P_CASE(false)
-#undef VC_ATTN3P_CASE
+  set_error("attention variant not built (tuning builds: VC_POLY_EVERY 0, 2, 3, 4)");
   return VC_EINVAL;
 }
 
@@ -847,10 +480,5 @@ template int launch_attn_tc3<64>(const AttnTcParams&, const void*, const void*, 
                                  int64_t, int64_t, cudaStream_t);
 template int launch_attn_tc3<80>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,
                                  int64_t, int64_t, cudaStream_t);
-
-template int launch_attn_tc3p<64>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,
-                                  int64_t, int64_t, cudaStream_t);
-template int launch_attn_tc3p<80>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t,
-                                  int64_t, int64_t, cudaStream_t);
 
 }  // namespace vc

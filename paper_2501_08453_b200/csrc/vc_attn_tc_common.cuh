@@ -1,4 +1,4 @@
-// Shared pieces of the tcgen05 attention kernels (vc_attn_tc.cu, vc_attn_tc2.cu):
+// Shared pieces of the tcgen05 attention kernels (vc_attn_tc.cu, vc_attn_tc3.cu):
 // Q/K smem descriptors, the per-row online-softmax step, O rescale, P store
 // and the output epilogue.  Thread = query row = TMEM lane throughout.
 #pragma once
@@ -181,48 +181,6 @@ __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr
           orow[d] = __float2bfloat16_rn(__uint_as_float(r[i]) * inv);
         }
       }
-    }
-  }
-}
-
-// Normalised O columns [16*C0, 16*C1) of one row -> a shared-memory staging
-// row (sdh = dh rounded up to even bf16, so every pair is 4-byte aligned).
-template <int DP, int C0, int C1>
-__device__ __forceinline__ void stage_out(uint32_t o_addr, float l, __nv_bfloat16* srow, int dh) {
-  const float inv = 1.f / l;
-#pragma unroll
-  for (int c = C0; c < C1; ++c) {
-    uint32_t r[16];
-    ptx::tmem_ld16(o_addr + c * 16, r);
-    ptx::tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 16; i += 2) {
-      const int d = c * 16 + i;
-      if (d < dh)
-        *reinterpret_cast<__nv_bfloat162*>(srow + d) =
-            __floats2bfloat162_rn(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv);
-    }
-  }
-}
-
-// Staged rows -> global, one warp per row: lanes write consecutive 4-byte
-// words, so a head row is one or two L2 lines per store instruction instead
-// of 32 rows per instruction (the per-thread store_out pattern).
-__device__ __forceinline__ void copy_out_rows(const AttnTcParams& p, const __nv_bfloat16* stg, int sdh, int qrow0,
-                                              int nrows, int seq, int h, int wi, int nw, int lane) {
-  if (!p.out) return;
-  for (int r = wi; r < nrows; r += nw) {
-    const int qi = qrow0 + r;
-    if (qi >= p.Lq) break;
-    __nv_bfloat16* orow = out_row(p, qi, seq, h);
-    const __nv_bfloat16* srow = stg + r * sdh;
-    if ((((uintptr_t)orow) & 3) == 0) {
-      const int nwd = p.dh >> 1;
-      for (int w = lane; w < nwd; w += 32)
-        reinterpret_cast<uint32_t*>(orow)[w] = reinterpret_cast<const uint32_t*>(srow)[w];
-      if ((p.dh & 1) && lane == 0) orow[p.dh - 1] = srow[p.dh - 1];
-    } else {
-      for (int d = lane; d < p.dh; d += 32) orow[d] = srow[d];
     }
   }
 }

@@ -13,6 +13,7 @@
 #include "vc_attn_tc.h"
 #include "vc_gemm_tc.h"
 #include "vc_kernels.h"
+#include "vc_tuning.h"
 
 namespace vc {
 
@@ -104,7 +105,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     g.qkv = sc; g.qkv.n_base = 0; g.qkv.text_rows = 0;
     // compact: 256-column tiles (the least-padding pick would be 176, whose
     // smaller tiles cost more than the 80 padding columns of 256)
-    static const int qkv_bn = getenv("VC_QKV_BN") ? atoi(getenv("VC_QKV_BN")) : 256;  // A/B
+    static const int qkv_bn = tuning_int("VC_QKV_BN", 256);  // A/B
     VC_TRY(launch_gemm_tc(xhat, D, wqkv, D, g, EPI_QKV, st, compact ? qkv_bn : 0));
   }
   if (compact) {  // V^T rows dh..DP-1 (ones column, zeros) the compact GEMM does not write

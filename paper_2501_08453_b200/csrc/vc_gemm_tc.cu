@@ -19,6 +19,7 @@
 //                sequence [seq][H][DP][keys] (the K-major B operand of P.V),
 //                temporal branch plain [row][3D].
 #include "vc_gemm_tc.h"
+#include "vc_tuning.h"
 #include "vc_ptx.cuh"
 
 namespace vc {
@@ -743,7 +744,7 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParams
     cfg.gridDim = dim3((unsigned)(num_sms() / CM * CM));
     if (cudaOccupancyMaxActiveClusters(&resident, gemm_tc_kernel<BN, EPI, CM>, &cfg) != cudaSuccess || resident <= 0)
       resident = num_sms() / CM;
-    if (getenv("VC_GEMM_DEBUG")) fprintf(stderr, "gemm_tc CM=%d: %d resident clusters\n", CM, resident);
+    if (tuning_debug()) fprintf(stderr, "gemm_tc CM=%d: %d resident clusters\n", CM, resident);
   }
   const int clusters = (int)std::min<int64_t>(ctiles, resident);
   cfg.gridDim = dim3((unsigned)(clusters * CM));
@@ -779,7 +780,7 @@ int launch_impl2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmTcParam
     if (cudaOccupancyMaxActiveClusters(&resident, gemm_tc2_kernel<BN, EPI, NP, EW>, &cfg) != cudaSuccess ||
         resident <= 0)
       resident = num_sms() / (2 * NP);
-    if (getenv("VC_GEMM_DEBUG")) fprintf(stderr, "gemm_tc2 NP=%d: %d resident clusters\n", NP, resident);
+    if (tuning_debug()) fprintf(stderr, "gemm_tc2 NP=%d: %d resident clusters\n", NP, resident);
   }
   const int clusters = (int)std::min<int64_t>(ctiles, resident);
   cfg.gridDim = dim3((unsigned)(clusters * 2 * NP));
@@ -917,23 +918,23 @@ int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const
               (long long)lda, (long long)ldb);
     return VC_EINVAL;
   }
-  static const int bn_env = getenv("VC_GEMM_BN") ? atoi(getenv("VC_GEMM_BN")) : 0;  // tuning switch
+  static const int bn_env = tuning_int("VC_GEMM_BN", 0);  // tuning switch
   // pairs per cluster: 2 sharing A by multicast for the O GEMM (EPI_F32:
   // 0.245 vs 0.264 ms), 1 for the QKV GEMM (0.94 vs 0.98: only 33 clusters of
   // 4 fit at once, 132 of 148 SMs, which eats the L2 saving); VC_GEMM_NP
   // overrides.  (Before the grid was sized with cudaOccupancyMaxActiveClusters
   // the 4-CTA clusters ran in two waves and looked 1.7x slower.)
-  static const int np_env = getenv("VC_GEMM_NP") ? atoi(getenv("VC_GEMM_NP")) : 0;
+  static const int np_env = tuning_int("VC_GEMM_NP", 0);
   // epilogue warps of the QKV scatter (8 default; VC_GEMM_EW=4 is the A/B switch)
-  static const int ew = getenv("VC_GEMM_EW") ? atoi(getenv("VC_GEMM_EW")) : 8;
+  static const int ew = tuning_int("VC_GEMM_EW", 8);
   // 2-CTA clusters along M multicast the B tile (halves its L2 traffic);
   // VC_GEMM_NO_MC=1 forces the single-CTA kernel (A/B switch for profiling).
-  static const bool no_mc = getenv("VC_GEMM_NO_MC") != nullptr;
+  static const bool no_mc = tuning_int("VC_GEMM_NO_MC", 0) != 0;
   // default: CTA-pair kernel (cta_group::2, 256-row tiles); VC_GEMM_1SM=1
   // selects the single-CTA kernel with B multicast (A/B switch for profiling)
-  static const bool one_sm = getenv("VC_GEMM_1SM") != nullptr;
+  static const bool one_sm = tuning_int("VC_GEMM_1SM", 0) != 0;
   const bool pair = !one_sm && epi != EPI_BF16 && cdiv(p.M, BM) >= 2;
-  static const int cm_env = getenv("VC_GEMM_CM") ? atoi(getenv("VC_GEMM_CM")) : 2;  // 1-CTA kernel cluster
+  static const int cm_env = tuning_int("VC_GEMM_CM", 2);  // 1-CTA kernel cluster
   const int cm = (!no_mc && epi != EPI_BF16 && cdiv(p.M, BM) >= 2) ? (cm_env == 4 && cdiv(p.M, BM) >= 4 ? 4 : 2) : 1;
   const int np_want = np_env ? np_env : (epi == EPI_F32 ? 2 : 1);
   if (bn == 0) bn = bn_env ? bn_env : gemm_tc_pick_bn(p.N, pair && np_want == 2 ? 2 : 1);

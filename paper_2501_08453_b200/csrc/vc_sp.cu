@@ -49,10 +49,16 @@ struct Sp {
   QkvPad pad;
 };
 
-int sp_make(const vc_sp_plan* pl, Sp* o, bool gather = false) {
+// counts_only: the exchange sizes are integer formulas; they are also asked
+// for shapes the bf16 kernels do not take (the reference's D = 12 toy plans)
+int sp_make(const vc_sp_plan* pl, Sp* o, bool gather = false, bool counts_only = false) {
   if (!pl) { set_error("null plan"); return VC_EINVAL; }
   const vc_block_shape& s = pl->shape;
-  VC_TRY(vc_block_shape_check(&s));
+  if (!counts_only) VC_TRY(vc_block_shape_check(&s));
+  else if (s.frames <= 0 || s.visual_len <= 0 || s.dim <= 0 || s.heads <= 0 || s.dim % s.heads) {
+    set_error("bad block shape");
+    return VC_EINVAL;
+  }
   if (s.dtype != VC_DTYPE_BF16) { set_error("sequence parallelism runs the bf16 path"); return VC_ENOTSUP; }
   const int P = pl->nranks;
   if (P < 1 || P > 16 || pl->rank < 0 || pl->rank >= P) {
@@ -373,13 +379,20 @@ size_t vc_sp_workspace_bytes(const vc_sp_plan* plan) {
 
 int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which, int32_t peer) {
   Sp x;
-  if (sp_make(plan, &x) != VC_OK || peer < 0 || peer >= x.P) return -1;
+  if (sp_make(plan, &x, false, which >= 4) != VC_OK || peer < 0 || peer >= x.P) return -1;
   const int64_t me = x.M[x.rank];
   switch (which) {
     case 0: return 6 * me * x.Hg * x.DP;           // send1 to peer (my rows, peer's heads)
     case 1: return 6 * x.M[peer] * x.Hg * x.DP;    // recv1 from peer (peer's rows, my heads)
     case 2: return 2 * x.M[peer] * x.Dg;           // send2 to peer (peer's rows, my heads)
     case 3: return 2 * me * x.Dg;                  // recv2 from peer (my rows, peer's heads)
+    // the same exchanges without the layout padding (head dim dh, not DP;
+    // head-group width Hg*dh, not the head slots): the reference's payload
+    // (executor.py:344-347, :395-412), for the byte accounting
+    case 4: return 6 * me * x.Hg * x.dh;
+    case 5: return 6 * x.M[peer] * x.Hg * x.dh;
+    case 6: return 2 * x.M[peer] * x.Hg * x.dh;
+    case 7: return 2 * me * x.Hg * x.dh;
   }
   return -1;
 }

@@ -82,10 +82,9 @@ def price_sp_block(stage_ms: dict, frames: int, visual_len: int, text_len: int, 
     head_share = 1.0 / p
     compute = {k: v * (row_share if k in _ROW_STAGES else head_share if k in _HEAD_STAGES else 1.0)
                for k, v in stage_ms.items()}
-    dpad = head_pad(dim // heads)
     # slowest rank's bytes: the one with the most rows sends/receives most
     r_max = max(range(p), key=lambda r: vb[r + 1] - vb[r])
-    c = exchange_counts(frames, visual_len, heads, dim, p, r_max, dpad)
+    c = exchange_counts(frames, visual_len, heads, dim, p, r_max)
     a2a1 = sum(c["send1"]) * 2.0 / 2   # bytes per branch (bf16, branch-major halves)
     a2a2 = sum(c["recv2"]) * 2.0 / 2
     t1 = alltoall_time(p, a2a1, spec.intra_bw, spec.alpha) * 1e3   # ms per branch

@@ -76,24 +76,24 @@ def check_plan(frames, visual_len, heads, p):
         raise ValueError(f"head-parallel attention needs sp_size to divide {heads} heads, got {p}")
 
 
-def exchange_counts(frames, visual_len, heads, dim, p, rank, head_pad):
-    """Per-peer element counts of the two all-to-alls (bf16 elements):
+def exchange_counts(frames, visual_len, heads, dim, p, rank, padded=True):
+    """Per-peer element counts of the two all-to-alls (bf16 elements), from
+    the C ABI (vc_sp_exchange_elems) so the layout rule lives in one place:
     send1/recv1 carry q,k,v of 2 branches for H/P heads (head dim padded to
-    head_pad); send2/recv2 carry 2 branches' attention outputs (H/P * dh, or
-    H/P head_pad-wide head slots when dh is 66).
+    DP); send2/recv2 carry 2 branches' attention outputs (H/P * dh, or H/P
+    DP-wide head slots when dh is 66). padded=False gives the same exchanges
+    without the layout padding (the reference's payload).
     The buffers are branch-major (vc_sp.cu): each branch is one half, split by
     peer with half these counts (branch_counts)."""
-    vb = contiguous_bounds(visual_len, p)
-    M = [frames * (vb[r + 1] - vb[r]) for r in range(p)]
-    # dh 66 (the 2B shape): outputs travel in head_pad-wide head slots (vc_sp.cu Sp.S)
-    hg = heads // p
-    dg = hg * (head_pad if dim // heads == 66 else dim // heads)
-    return {
-        "send1": [6 * M[rank] * hg * head_pad for _ in range(p)],
-        "recv1": [6 * M[r] * hg * head_pad for r in range(p)],
-        "send2": [2 * M[r] * dg for r in range(p)],
-        "recv2": [2 * M[rank] * dg for _ in range(p)],
-    }
+    lib = _lib.load()
+    plan = _lib.SpPlan(_lib.shape(frames, visual_len, 0, dim, heads, "bf16"), p, rank)
+    base = 0 if padded else 4
+    out = {}
+    for i, k in enumerate(("send1", "recv1", "send2", "recv2")):
+        out[k] = [int(lib.vc_sp_exchange_elems(C.byref(plan), base + i, r)) for r in range(p)]
+        if min(out[k]) < 0:
+            raise ValueError(lib.vc_last_error().decode())
+    return out
 
 
 def branch_counts(counts):

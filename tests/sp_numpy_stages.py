@@ -28,7 +28,7 @@ class NumpyStages:
         self.DP = sp.head_pad(self.dh)
         self.vb = sp.contiguous_bounds(Lv, P)
         self.M = [F * (self.vb[r + 1] - self.vb[r]) for r in range(P)]
-        self.counts = sp.exchange_counts(F, Lv, H, D, P, rank, self.DP)
+        self.counts = sp.exchange_counts(F, Lv, H, D, P, rank)
         mk = lambda k: torch.zeros(sum(self.counts[k]), dtype=torch.float64)  # noqa: E731
         self.send1, self.recv1, self.send2, self.recv2 = mk("send1"), mk("recv1"), mk("send2"), mk("recv2")
 

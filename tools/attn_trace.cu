@@ -1,5 +1,5 @@
-// Standalone timing + per-phase trace of the ping-pong tcgen05 attention
-// kernel (vc_attn_tc2.cu) on the config-2 full-sequence shape.  Built by
+// Standalone timing + per-phase trace of the tcgen05 attention kernel
+// (vc_attn_tc3.cu) on the config-2 full-sequence shape.  Built by
 // tools/build_attn_trace.sh with -DVC_ATTN_TRACE (the trace writes clock64()
 // stamps of one CTA into a __device__ array; the library build has none).
 //
@@ -14,7 +14,6 @@
 #include "../paper_2501_08453_b200/csrc/vc_attn_tc.h"
 
 namespace vc {
-int attn_trace_read(unsigned long long* host);
 int attn_trace3_read(unsigned long long* host);
 }
 
@@ -62,11 +61,10 @@ int main(int argc, char** argv) {
   const double flop = 4.0 * Lq * (double)Lk * H * dh;
   printf("# Lq %d Lk %d H %d dh %d DP %d: %.4f ms  %.1f TFLOP/s (algorithmic dh)\n", Lq, Lk, H, dh, DP, ms,
          flop / ms / 1e9);
-  const int impl = getenv("VC_ATTN_IMPL") ? atoi(getenv("VC_ATTN_IMPL")) : 3;
-  const int nroles = impl == 2 ? 3 : 17;
+  const int nroles = 17;
   const int nj = 256;
   std::vector<unsigned long long> tr(17 * 512 * 8);
-  const int trc = impl == 2 ? vc::attn_trace_read(tr.data()) : vc::attn_trace3_read(tr.data());
+  const int trc = vc::attn_trace3_read(tr.data());
   if (trc == 0) {
     unsigned long long t0 = ~0ull;
     for (auto v : tr) if (v && v < t0) t0 = v;
