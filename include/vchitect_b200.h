@@ -227,6 +227,13 @@ VC_API size_t vc_sp_workspace_bytes(const vc_sp_plan* plan);
  * peer (bf16 elements as laid out: head dim padded to DP, dh-66 outputs in
  * DP-wide head slots); 4..7 the same without that padding (the reference's
  * payload, executor.py:344-347, :395-412). -1 on error. */
+/* The row maps the exchanges use (exact-equality tests against the
+ * reference's stable argsort, executor.py:349-370, :606-617). which 0: for
+ * the rows of every rank concatenated in rank order (each rank's local rows
+ * frame-major), the visual token f*Lv + l the a2a #1 unpack assembles them
+ * as (F*Lv entries); which 1: for each visual token, the index of the row it
+ * is returned to by a2a #2 in that same concatenation. Host only. */
+VC_API int vc_sp_row_map(const vc_sp_plan* plan, int32_t which, int64_t* out);
 VC_API int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which,
                                     int32_t peer);
 /* x_local [F][vc_r][D] fp32, prompt [Lt][D] fp32 -> send1 (bf16). */

@@ -251,6 +251,65 @@ def parallel_block_forward(block, visual, text, heads):
             + full_sequence_attention(block.fullseq, text, visual, heads))
 
 
+def _rows_attention(q, k, v, heads, chunk=32):
+    """attention() for a few query rows against many keys, query-chunked so
+    the [rows, keys] scores of all heads stay small (numerics.py:87-107)."""
+    out = np.empty_like(q)
+    for i in range(0, q.shape[0], chunk):
+        out[i:i + chunk] = attention(q[i:i + chunk], k, v, heads)
+    return out
+
+
+def parallel_block_rows(block, visual, text, heads, f_idx, l_idx):
+    """Rows (f_idx[i], l_idx[i]) of each branch of parallel_block_forward
+    (model.py:263-271), computed for just those query rows: every key and
+    value the rows attend to is projected (all Lv rows of a sampled frame for
+    the spatial branch, model.py:230-235; all F frames of a sampled position
+    for the temporal branch, model.py:238-244; the whole anchored
+    checkerboard sequence, F literal copies of text[0] included, for the
+    full-sequence branch, model.py:247-260), queries and the O projection
+    only for the sampled rows. Returns {"spatial", "temporal", "fullseq",
+    "block"}: [n, D] each. Same arithmetic per row as the full forward, so it
+    is checked against parallel_block_forward on small shapes
+    (tests/test_oracle_golden.py) and used at the full BASELINE shapes where
+    the full fp64 forward does not fit a test's time budget."""
+    f_idx = np.asarray(f_idx, dtype=np.int64)
+    l_idx = np.asarray(l_idx, dtype=np.int64)
+    frames, lv, d = visual.shape
+    n = f_idx.size
+    out = {k: np.zeros((n, d)) for k in ("spatial", "temporal", "fullseq")}
+    # spatial: one sequence per frame
+    p = block.spatial
+    for f in np.unique(f_idx):
+        sel = np.nonzero(f_idx == f)[0]
+        q, _, _ = branch_qkv(p, visual[f, l_idx[sel]])
+        _, k, v = branch_qkv(p, visual[f])
+        out["spatial"][sel] = _rows_attention(q, k, v, heads) @ p.wo
+    # temporal: one sequence per spatial position
+    p = block.temporal
+    for pos in np.unique(l_idx):
+        sel = np.nonzero(l_idx == pos)[0]
+        q, _, _ = branch_qkv(p, visual[f_idx[sel], pos])
+        _, k, v = branch_qkv(p, visual[:, pos])
+        out["temporal"][sel] = _rows_attention(q, k, v, heads) @ p.wo
+    # full sequence: [t0 v0 t1 v1 ...] with every text slot = text[0]
+    p = block.fullseq
+    lt = text.shape[1]
+    _, kt, vt = branch_qkv(p, text[0])
+    kv = np.empty((frames, lv, d))
+    vv = np.empty((frames, lv, d))
+    for f in range(frames):  # frame by frame: the whole clip at once doubles the peak memory
+        _, kv[f], vv[f] = branch_qkv(p, visual[f])
+    k = np.concatenate([np.broadcast_to(kt, (frames, lt, d)), kv], axis=1).reshape(-1, d)
+    del kv
+    v = np.concatenate([np.broadcast_to(vt, (frames, lt, d)), vv], axis=1).reshape(-1, d)
+    del vv
+    q, _, _ = branch_qkv(p, visual[f_idx, l_idx])
+    out["fullseq"] = _rows_attention(q, k, v, heads) @ p.wo
+    out["block"] = out["spatial"] + out["temporal"] + out["fullseq"]
+    return out
+
+
 @dataclass
 class ToyDenoiser:
     """model.py:274-333."""

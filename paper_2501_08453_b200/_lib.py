@@ -65,6 +65,7 @@ SIGNATURES = {
     "vc_sp_bounds": (C.c_int, [C.POINTER(SpPlan), C.POINTER(C.c_int32)]),
     "vc_sp_workspace_bytes": (_sz, [C.POINTER(SpPlan)]),
     "vc_sp_exchange_elems": (_i64, [C.POINTER(SpPlan), _i32, _i32]),
+    "vc_sp_row_map": (_i32, [C.POINTER(SpPlan), _i32, C.c_void_p]),
     "vc_sp_stage1": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _p, _sz, _p]),
     "vc_sp_stage2": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _sz, _p]),
     "vc_sp_stage2_branch": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _i32, _p, _sz, _p]),

@@ -7,6 +7,7 @@
 #include "vc_attn_tc.h"
 #include "vc_gemm_tc.h"
 #include "vc_ptx.cuh"
+#include "vc_sp_maps.cuh"
 
 namespace vc {
 namespace attn {
@@ -125,11 +126,9 @@ __device__ __forceinline__ __nv_bfloat16* out_row(const AttnTcParams& p, int qi,
            (int64_t)h * (p.head_slot ? p.head_slot : p.dh);
   const int f = p.spo.branch == 0 ? seq : qi / p.spo.Lv;
   const int lpos = p.spo.branch == 0 ? qi : qi - f * p.spo.Lv;
-  int r = 0;
-  while (r + 1 < p.spo.P && p.spo.vb[r + 1] <= lpos) ++r;
-  const int vc = p.spo.vb[r + 1] - p.spo.vb[r];
+  const int r = sp_owner(p.spo.vb, p.spo.P, lpos);
   // base[r] already points at this branch's block for rank r
-  return p.out + p.spo.base[r] + ((int64_t)f * vc + (lpos - p.spo.vb[r])) * p.spo.Dg +
+  return p.out + p.spo.base[r] + sp_token_to_row(p.spo.vb, r, f, lpos) * p.spo.Dg +
          (int64_t)h * (p.head_slot ? p.head_slot : p.dh);
 }
 

@@ -26,6 +26,7 @@
 #include "vc_attn_tc.h"
 #include "vc_gemm_tc.h"
 #include "vc_kernels.h"
+#include "vc_sp_maps.cuh"
 
 namespace vc {
 
@@ -165,7 +166,8 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
       for (int rr = 0; rr < 32; ++rr) {
         const int64_t m = m0 + rr;
         if (m >= Mr) break;
-        const int f = (int)(m / vc), l = a.vb[r] + (int)(m - (int64_t)f * vc);
+        int f, l;
+        sp_row_to_token(a.vb, r, m, f, l);
         const int64_t tok = (int64_t)f * a.Lv + l;
         const uint4* s4 = reinterpret_cast<const uint4*>(a.recv + a.off[r] + ((int64_t)blk * Mr + m) * rowlen);
         __nv_bfloat16* dst;
@@ -187,7 +189,8 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
     }
     const int64_t m = (wl - which * gpb) * 32 + lane;
     if (m >= Mr) continue;
-    const int f = (int)(m / vc), l = a.vb[r] + (int)(m - (int64_t)f * vc);
+    int f, l;
+    sp_row_to_token(a.vb, r, m, f, l);
     const __nv_bfloat16* src = a.recv + a.off[r] + ((int64_t)blk * Mr + m) * rowlen;
     const int64_t tok = (int64_t)f * a.Lv + l;  // visual token index
     if (which < 2) {
@@ -310,10 +313,8 @@ __global__ void __launch_bounds__(256) spg_unpack_k_kernel(SpgUnpack a) {
     const int b = (int)(w / ((int64_t)a.F * a.Lv));   // 0 spatial, 1 full sequence
     const int64_t tok = w - (int64_t)b * a.F * a.Lv;   // global visual token f*Lv + l
     const int f = (int)(tok / a.Lv), l = (int)(tok - (int64_t)f * a.Lv);
-    int r = 0;
-    while (l >= a.vb[r + 1]) ++r;
-    const int vc = a.vb[r + 1] - a.vb[r];
-    const int64_t m = (int64_t)f * vc + (l - a.vb[r]);
+    const int r = sp_owner(a.vb, a.P, l);
+    const int64_t m = sp_token_to_row(a.vb, r, f, l);
     const uint4* src = reinterpret_cast<const uint4*>(a.gather + r * a.slot + (b == 0 ? a.offA : a.offC) +
                                                       m * a.H * a.DP);
     uint4* dst = reinterpret_cast<uint4*>(b == 0 ? a.ksp + tok * a.H * a.DP : a.kfs + (a.Lt + tok) * a.H * a.DP);
@@ -395,6 +396,31 @@ int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which, int32_t peer
     case 7: return 2 * me * x.Hg * x.dh;
   }
   return -1;
+}
+
+int vc_sp_row_map(const vc_sp_plan* plan, int32_t which, int64_t* out) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x, false, true));
+  if (!out || which < 0 || which > 1) { set_error("vc_sp_row_map: which must be 0 or 1"); return VC_EINVAL; }
+  if (which == 0) {  // recv rows (source rank, local row) -> visual token, as sp_unpack1 places them
+    int64_t i = 0;
+    for (int r = 0; r < x.P; ++r)
+      for (int64_t m = 0; m < x.M[r]; ++m) {
+        int f, l;
+        sp_row_to_token(x.vb, r, m, f, l);
+        out[i++] = (int64_t)f * x.Lv + l;
+      }
+  } else {  // visual token -> (owner rank, local row) as one index into the rank-ordered row list (out_row)
+    int64_t first[17];
+    first[0] = 0;
+    for (int r = 0; r < x.P; ++r) first[r + 1] = first[r] + x.M[r];
+    for (int f = 0; f < x.F; ++f)
+      for (int l = 0; l < x.Lv; ++l) {
+        const int r = sp_owner(x.vb, (int)x.P, l);
+        out[(int64_t)f * x.Lv + l] = first[r] + sp_token_to_row(x.vb, r, f, l);
+      }
+  }
+  return VC_OK;
 }
 
 int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_local, const float* prompt,

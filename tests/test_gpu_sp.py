@@ -24,8 +24,9 @@ def torch():
 
 
 @pytest.mark.parametrize("shape,Ps", [((3, 64, 32, 256, 8), (1, 2, 4, 8)),
-                                      ((2, 1350, 256, 1584, 24), (2, 3, 8))],
-                         ids=["small_dh32", "2b_f2"])
+                                      ((2, 1350, 256, 1584, 24), (2, 3, 8)),
+                                      ((2, 96, 32, 1024, 8), (2, 4, 8))],
+                         ids=["small_dh32", "2b_f2", "dh128"])
 def test_sp_matches_single_gpu_and_oracle(torch, shape, Ps):
     import paper_2501_08453_b200 as vc
     from paper_2501_08453_b200 import sp

@@ -106,3 +106,51 @@ def test_plan_validity_errors_match_reference_wording():
         sp.check_plan(2, 3, 8, 4)
     with pytest.raises(ValueError, match="divide"):
         sp.check_plan(2, 30, 6, 4)
+
+
+def _row_map(F, Lv, Lt, D, H, P, which):
+    lib = _lib.load()
+    plan = _lib.SpPlan(_lib.shape(F, Lv, Lt, D, H, "bf16"), P, 0)
+    out = np.empty(F * Lv, dtype=np.int64)
+    assert lib.vc_sp_row_map(C.byref(plan), which, out.ctypes.data) == 0, lib.vc_last_error()
+    return out
+
+
+@pytest.mark.parametrize("P", [3, 8])
+def test_sp_reassembly_order_equals_reference_stable_argsort(P):
+    # north star: exact equality on the token-shard and index permutations.
+    # The reference assembles every sequence from the devices' chunks with a
+    # stable argsort of their global indices (executor.py:349-370; spatial
+    # chunks :571-590 carry the positions of one frame, full-sequence chunks
+    # :606-617 the interleaved text + visual indices). The product's row map
+    # (vc_sp_row_map, the function sp_unpack1 / the attention epilogue use)
+    # must put every received row exactly where that argsort puts it.
+    from oracle import spsim_oracle as O
+    F, Lv, Lt, D, H = 16, 1350, 256, 1584, 24
+    tok = _row_map(F, Lv, Lt, D, H, P, 0)      # concatenated (rank, local row) -> f*Lv + l
+    vb = O.contiguous_bounds(Lv, P)
+    # spatial branch: per frame, the chunks' position indices in device order
+    firsts = np.cumsum([0] + [F * (vb[r + 1] - vb[r]) for r in range(P)])
+    for f in range(F):
+        idx = np.concatenate([np.arange(vb[r], vb[r + 1]) for r in range(P)])
+        order = np.argsort(idx, kind="stable")
+        pos = np.empty_like(order)
+        pos[order] = np.arange(order.size)            # where the argsort puts each received row
+        ours = np.concatenate([tok[firsts[r] + f * (vb[r + 1] - vb[r]):firsts[r] + (f + 1) * (vb[r + 1] - vb[r])]
+                               for r in range(P)])
+        assert ours.tolist() == (f * Lv + pos).tolist()
+    # full sequence: the reference's interleaved global order; our key order
+    # is the deduplicated text first, then the visual tokens -- the visual
+    # rows must appear in the reference's relative order
+    idx_by_dev, order = O.fullseq_global_order(F, Lt, Lv, P)
+    idx = np.concatenate(idx_by_dev)
+    stride = Lt + Lv
+    is_vis = (idx % stride) >= Lt
+    ref_vis_rank = np.empty(idx.size, dtype=np.int64)
+    ranked = order[is_vis[order]]                     # visual rows in sorted order
+    ref_vis_rank[ranked] = np.arange(ranked.size)
+    assert tok.tolist() == ref_vis_rank[is_vis].tolist()
+    # a2a #2: every visual token goes back to exactly the row it came from
+    back = _row_map(F, Lv, Lt, D, H, P, 1)
+    assert np.array_equal(back[tok], np.arange(F * Lv))
+    assert sorted(back.tolist()) == list(range(F * Lv))
