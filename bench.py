@@ -63,6 +63,17 @@ def algorithmic_bytes(F, Lv, Lt, D, H):
     return {"ln": (Nv + Lt) * D * (4 + 2)}
 
 
+def tensor_peak(peaks, clocks):
+    """The bf16 roofline denominator for a kernel timed inside this run: the
+    burst peak when the SM clock stayed at its maximum through the timed
+    region (MEASURED_PEAKS.json bf16_tflops), the sustained one when it did
+    not (a power-capped multi-second run)."""
+    sm, mx = (clocks or {}).get("sm_mhz"), (clocks or {}).get("sm_max_mhz")
+    if sm and mx and sm >= 0.97 * mx:
+        return peaks["tc"], f"{peaks['src']} bf16 burst (SM clock at its maximum during the timed region)"
+    return peaks["tc_sus"], f"{peaks['src']} bf16 sustained (SM clock below its maximum during the timed region)"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -183,42 +194,40 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the pinned oracle port (fp64 numpy) on a bounded sample
+# CPU baseline: the pinned oracle port, exact frame slices of the block
 # ---------------------------------------------------------------------------
 
-def cpu_sample(cfg_id, sample_frames):
-    """Time the reference algorithm (oracle port) for a `sample_frames`-frame
-    clip of the config's geometry, branch by branch, and extrapolate to the
-    full clip with the reference's own cost scaling (spatial
-    and temporal proportional to F, full sequence to S^2, S = F (Lt + Lv))."""
+def cpu_slices(cfg_id, seed=2025):
+    """The reference block forward of the config's clip (oracle port, fp64),
+    ready to run frame slice by frame slice (oracle/frame_slices.py: F
+    consecutive slices are exactly one block forward's arithmetic)."""
     from oracle import spsim_oracle as O
+    from oracle.frame_slices import FrameSlices
     F, Lv, Lt, D, H, _ = CONFIGS[cfg_id]
-    Fs = min(sample_frames, F)
-    blk = O.BlockParams.init(O.SeededRng(2025).split(1000), D)
-    data = O.SeededRng(2025).split(1 << 20)
-    x = data.split(1).normal((Fs, Lv, D))
-    text = O.anchor_text(data.split(2).normal((Lt, D)), Fs)
-    t0 = time.perf_counter()
-    O.spatial_branch(blk.spatial, x, H)
-    t1 = time.perf_counter()
-    O.temporal_branch(blk.temporal, x, H)
-    t2 = time.perf_counter()
-    # full-sequence branch (model.py:247-260) timed in its linear part
-    # (LN + Q/K/V projections of all S rows, O projection) and its S^2 part
-    p = blk.fullseq
-    seq = O.interleave_checkerboard(text, x)
-    q, k, v = O.branch_qkv(p, seq)
-    t3 = time.perf_counter()
-    att = O.attention(q, k, v, H)
-    t4 = time.perf_counter()
-    O.deinterleave_visual(att @ p.wo, Fs, Lt, Lv)
-    t5 = time.perf_counter()
-    sp, tm = t1 - t0, t2 - t1
-    fs_lin, fs_quad = (t3 - t2) + (t5 - t4), t4 - t3
-    r = F / Fs
-    full = (sp + tm + fs_lin) * r + fs_quad * r * r
-    return {"sample_s": t5 - t0, "full_s": full, "tokens": F * Lv,
-            "value": F * Lv / full, "branches_s": [sp, tm, fs_lin, fs_quad], "Fs": Fs}
+    blk = O.BlockParams.init(O.SeededRng(seed).split(1000), D)
+    data = O.SeededRng(seed).split(1 << 20)
+    x = data.split(1).normal((F, Lv, D))
+    prompt = data.split(2).normal((Lt, D))
+    return FrameSlices(blk, x, prompt, H)
+
+
+def time_slices(fs, n, start=0):
+    """Run n consecutive frame slices; returns the per-slice seconds."""
+    out = []
+    for i in range(n):
+        t0 = time.perf_counter()
+        fs.step((start + i) % fs.F)
+        out.append(time.perf_counter() - t0)
+    return out
+
+
+def slice_sample_text(cfg_id, n):
+    F, Lv, Lt, D, H, name = CONFIGS[cfg_id]
+    return (f"oracle port of the reference block forward (fp64 numpy, pinned to the reference's golden outputs), "
+            f"{name}: {n} exact frame slices (one slice = 1/{F} of the block's arithmetic: frame f's spatial "
+            f"sequence, its rows' temporal queries against all {F} frames, its {Lt}+{Lv} full-sequence queries "
+            f"against all {F * (Lt + Lv)} keys, each slice re-projecting its own frame's K/V), "
+            f"{Lv} visual tokens per slice; tokens/s = slices x {Lv} / their total time")
 
 
 def cpu_cores():
@@ -232,29 +241,26 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
-    F, Lv, Lt, D, H, name = cfg
-    for _ in range(args.warmup):
-        cpu_sample(args.config, args.sample_frames)
-    vals, samples = [], []
-    for _ in range(args.steps):
-        r = cpu_sample(args.config, args.sample_frames)
-        vals.append(r["value"])
-        samples.append(r)
-    value = float(np.median(vals))
-    full_s = float(np.median([r["full_s"] for r in samples]))
-    sample = (f"oracle port (fp64 numpy, pinned to the reference's golden outputs) block forward of a "
-              f"{samples[0]['Fs']}-frame clip of {name}, branches timed and extrapolated to F={F} "
-              f"(spatial, temporal, full-seq projections ~F; full-seq attention ~F^2); median of {args.steps} steps")
+    if args.config not in CONFIGS:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the reference arm times block configs (1, 2, 4, 5); config 3 is a 40-block model step"}))
+        return
+    F, Lv, Lt, D, H, name = CONFIGS[args.config]
+    fs = cpu_slices(args.config)
+    time_slices(fs, args.warmup)
+    ts = time_slices(fs, args.steps, start=args.warmup)
+    total = float(sum(ts))
+    value = args.steps * Lv / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": full_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SeededRng)",
         "config": {"workload": name, "frames": F, "visual_len": Lv, "text_len": Lt, "dim": D,
-                   "heads": H},
+                   "heads": H, "tokens_per_step": Lv,
+                   "step": f"one exact 1/{F} frame slice of the block forward ({Lv} visual tokens)"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
-                         "sample": sample},
+                         "sample": slice_sample_text(args.config, args.steps)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -384,13 +390,14 @@ def run_gpu_arm(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        r = cpu_sample(args.config, args.sample_frames)
-        cpu = {"value": r["value"], "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
-               "sample": (f"oracle port (fp64 numpy, pinned to reference golden outputs), {r['Fs']}-frame clip "
-                          f"of the same geometry ({r['sample_s']:.1f} s), branches extrapolated to F={F} "
-                          f"(spatial, temporal, full-seq projections ~F; full-seq attention ~F^2)")}
+        fs = cpu_slices(args.config)
+        ts = time_slices(fs, 2)
+        cpu = {"value": 2 * Lv / sum(ts), "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+               "sample": slice_sample_text(args.config, 2)}
 
     launches = lib.vc_block_forward_launches(C.byref(shp)) * args.steps
+    clocks = clk.summary()
+    peak, peak_kind = tensor_peak(peaks, clocks)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -400,12 +407,13 @@ def run_gpu_arm(args):
                    "heads": H, "tokens_per_step": Nv, "parallelism": "single GPU",
                    "l2": "inputs larger than L2 (x fp32 %.0f MB + weights %.0f MB > 126 MB)"
                    % (Nv * D * 4 / 1e6, db.packed.numel() / 1e6)},
-        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["tc_sus"],
-                     "unit": "TFLOP/s", "frac": achieved / peaks["tc_sus"], "traffic": traffic,
-                     "peak_kind": f"{peaks['src']} bf16 sustained (kernel timed inside a long step)",
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "share_of_step": stages[dom] / sum(stages.values())},
         "block": {"tflops_algorithmic": block_tflops, "frac_of_bf16_peak": block_tflops / peaks["tc"],
-                  "stage_ms": stages},
+                  "frac_of_bf16_sustained": block_tflops / peaks["tc_sus"],
+                  "peak_note": "frac_of_bf16_peak is against the burst peak (MEASURED_PEAKS.json bf16_tflops)",
+                  "stage_ms": stages, "stage_sum_ms": sum(stages.values())},
         "cpu_baseline": cpu,
         "e2e": {"value": Nv / (e2e_ms / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": Nv * D * 4, "d2h_bytes_per_step": Nv * D * 4,
@@ -413,7 +421,7 @@ def run_gpu_arm(args):
                        "the device-resident weight handle, %d steps in one call, pinned host in/out, copies "
                        "overlapped across steps (pipeline fill + drain inside the timed region)" % args.steps,
                 "single_call_tokens_per_s": Nv / (single_host_ms / 1e3) if single_host_ms else None},
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "gpu_launches": launches,
     }
     print(json.dumps(line), flush=True)
@@ -467,6 +475,8 @@ def run_model_step(args, torch, world, rank, local):
     assert torch.isfinite(eps).all().item()
     flops = depth * sum(algorithmic_flops(F, Lv, Lt, D, H).values())
     peaks = load_peaks()
+    clocks = clk.summary()
+    peak, peak_kind = tensor_peak(peaks, clocks)
     if rank == 0:
         line = {
             "metric": METRIC, "value": Nv / (ms_per_step / 1e3), "unit": "tokens/s", "n_gpus": world,
@@ -476,10 +486,10 @@ def run_model_step(args, torch, world, rank, local):
             "config": {"workload": name, "frames": F, "visual_len": Lv, "text_len": Lt, "dim": D, "heads": H,
                        "depth": depth, "tokens_per_step": Nv, "parallelism": par},
             "roofline": {"bound": "tensor", "kernel": "whole model step (per GPU)",
-                         "achieved": flops / world / (ms_per_step / 1e3) / 1e12, "peak": peaks["tc_sus"],
-                         "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peaks["tc_sus"],
-                         "traffic": None},
-            "cpu_baseline": None, "e2e": None, "clocks": clk.summary(), "gpu_launches": None,
+                         "achieved": flops / world / (ms_per_step / 1e3) / 1e12, "peak": peak,
+                         "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peak,
+                         "traffic": None, "peak_kind": peak_kind},
+            "cpu_baseline": None, "e2e": None, "clocks": clocks, "gpu_launches": None,
         }
         print(json.dumps(line), flush=True)
     if world > 1 or args.sp:
@@ -490,7 +500,8 @@ def run_model_step(args, torch, world, rank, local):
 def run_gpu_sp(args, torch, world, rank, local):
     from paper_2501_08453_b200 import sp
     return sp.bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops,
-                       load_peaks, ClockSampler, cpu_sample, cpu_cores)
+                       load_peaks, tensor_peak, ClockSampler, cpu_slices, time_slices, slice_sample_text,
+                       cpu_cores)
 
 
 def main():
@@ -512,7 +523,26 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_gpu_arm(args)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N
+    ranks, one per GPU (torch.distributed.run, 127.0.0.1 rendezvous); rank 0
+    prints the line."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} GPU(s) visible")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
 
 
 if __name__ == "__main__":

@@ -463,8 +463,31 @@ def sp_model_forward(torch, model, latents, t, prompt, spb_cache, exchange, rank
 # bench.py --gpus N (torchrun, one rank per GPU)
 # ---------------------------------------------------------------------------
 
-def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops, load_peaks,
-             ClockSampler, cpu_sample, cpu_cores):
+def time_exchanges(torch, spb, ex, reps=5):
+    """Each branch's two all-to-alls timed ALONE (not overlapped), with CUDA
+    events on the current stream around a blocking all_to_all_single (the
+    current stream waits for NCCL's stream, so the interval is the
+    collective). Returns {name: ms} per rank."""
+    bc = branch_counts(spb.counts)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {}
+    for b, bn in ((0, "spatial"), (1, "fullseq")):
+        for send, recv, sc, rc, tag in (("send1", "recv1", "send1", "recv1", "a2a1"),
+                                        ("send2", "recv2", "send2", "recv2", "a2a2")):
+            args = (_half(getattr(spb, recv), b), _half(getattr(spb, send), b), bc[rc], bc[sc])
+            ex.all_to_all(*args)  # warm
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                ex.all_to_all(*args)
+            e1.record()
+            torch.cuda.synchronize()
+            out[f"{bn}_{tag}"] = e0.elapsed_time(e1) / reps
+    return out
+
+
+def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops, load_peaks, tensor_peak,
+             ClockSampler, cpu_slices, time_slices, slice_sample_text, cpu_cores):
     import json
     import torch.distributed as dist
 
@@ -533,12 +556,43 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
     torch.cuda.synchronize()
     e2e = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    # the exchanges alone (untimed pass): NVLink GB/s per rank, max time over ranks
+    a2a = {"mode": mode}
+    if mode == "head_parallel":
+        t = time_exchanges(torch, spb, ex)
+        tt = torch.tensor([t[k] for k in sorted(t)], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = dict(zip(sorted(t), tt.tolist()))
+        bc = branch_counts(spb.counts)
+        ref = branch_counts(exchange_counts(F, Lv, H, D, world, rank, padded=False))
+        for k, ms_k in t.items():
+            tag = "send1" if k.endswith("a2a1") else "send2"
+            # bytes leaving this rank over NVLink (its own block stays local)
+            wire = 2 * (sum(bc[tag]) - bc[tag][rank])
+            alg = 2 * (sum(ref[tag]) - ref[tag][rank])
+            a2a[k] = {"ms": ms_k, "nvlink_bytes_per_rank": wire, "nvlink_gbs": wire / (ms_k / 1e3) / 1e9,
+                      "algorithmic_bytes_per_rank": alg,
+                      "algorithmic_gbs": alg / (ms_k / 1e3) / 1e9}
+        a2a["note"] = ("each all-to-all timed alone (blocking, CUDA events, max over ranks); in the block "
+                       "step they overlap attention (sp.run_stages). nvlink_bytes = what this rank sends to "
+                       "its peers as laid out (head dim padded 66 -> 80); algorithmic = the reference's "
+                       "payload (executor.py:344-347, :395-412). At 1 rank every exchange is a local copy.")
+    else:  # bf16 bytes sent per rank: own slot to every peer
+        a2a["bytes_sent_per_rank_per_step"] = 2 * spb.slot * (world - 1)
     flops = sum(algorithmic_flops(F, Lv, Lt, D, H).values())
     peaks = load_peaks()
-    if mode == "gather":  # bf16 bytes sent per rank: own slot to every peer
-        a2a_bytes = 2 * spb.slot * (world - 1)
-    else:
-        a2a_bytes = 2 * (sum(spb.counts["send1"]) + sum(spb.counts["send2"]))
+    clocks = clk.summary()
+    all_clocks = [None] * world
+    dist.all_gather_object(all_clocks, clocks)
+    # the bound for every rank: burst only if every rank stayed at its max clock
+    peak_kinds = [tensor_peak(peaks, c) for c in all_clocks]
+    peak, peak_kind = min(peak_kinds)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        fs = cpu_slices(args.config)
+        ts = time_slices(fs, 2)
+        cpu = {"value": 2 * Lv / sum(ts), "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+               "sample": slice_sample_text(args.config, 2)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -552,14 +606,15 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
                                        + ", NCCL)"),
                        "l2": "inputs larger than L2 on every rank"},
             "roofline": {"bound": "tensor", "kernel": "whole block (per GPU)",
-                         "achieved": flops / world / (ms_per_step / 1e3) / 1e12, "peak": peaks["tc_sus"],
-                         "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peaks["tc_sus"],
-                         "traffic": None},
-            "a2a": {"mode": mode, "bytes_sent_per_rank_per_step": a2a_bytes},
-            "cpu_baseline": None,
+                         "achieved": flops / world / (ms_per_step / 1e3) / 1e12, "peak": peak,
+                         "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peak,
+                         "traffic": None, "peak_kind": peak_kind},
+            "a2a": a2a,
+            "cpu_baseline": cpu,
             "e2e": {"value": Nv / (float(e2e.item()) / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(xh.numel() * 4) * world, "d2h_bytes_per_step": int(oh.numel() * 4) * world},
-            "clocks": clk.summary(),
+            "clocks": clocks,
+            "clocks_per_rank": all_clocks,
             "gpu_launches": spb.launches_per_forward() * args.steps,
         }
         print(json.dumps(line), flush=True)

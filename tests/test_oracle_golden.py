@@ -129,3 +129,34 @@ def test_patchify_round_trip_and_order():
     r = O.SeededRng(2).normal((5, 3, 2))
     assert np.array_equal(O.unpatchify(O.patchify(r, 2), 5, 3, 2, 2), r)
     assert O.seq_len(144, 1920, 1080) == 1_175_040
+
+
+def test_row_oracle_equals_full_forward():
+    # oracle.parallel_block_rows (used at the full BASELINE shapes on sampled
+    # rows) is the same computation as the golden-pinned full forward
+    F, Lv, Lt, D, H = 5, 37, 6, 48, 4
+    blk = O.BlockParams.init(O.SeededRng(5).split(1000), D)
+    x = O.SeededRng(6).normal((F, Lv, D))
+    text = O.anchor_text(O.SeededRng(7).normal((Lt, D)), F)
+    fi = np.array([0, 4, 2, 2, 0, 3])
+    li = np.array([0, 36, 5, 17, 36, 1])
+    rows = O.parallel_block_rows(blk, x, text, H, fi, li)
+    np.testing.assert_allclose(rows["block"], O.parallel_block_forward(blk, x, text, H)[fi, li], atol=1e-12)
+    np.testing.assert_allclose(rows["spatial"], O.spatial_branch(blk.spatial, x, H)[fi, li], atol=1e-12)
+    np.testing.assert_allclose(rows["temporal"], O.temporal_branch(blk.temporal, x, H)[fi, li], atol=1e-12)
+    np.testing.assert_allclose(rows["fullseq"], O.full_sequence_attention(blk.fullseq, text, x, H)[fi, li],
+                               atol=1e-12)
+
+
+def test_frame_slices_equal_full_forward():
+    # bench.py's reference arm times these slices; F of them are exactly one
+    # block forward (oracle/frame_slices.py)
+    from oracle.frame_slices import FrameSlices
+    F, Lv, Lt, D, H = 4, 21, 5, 48, 4
+    blk = O.BlockParams.init(O.SeededRng(8).split(1000), D)
+    x = O.SeededRng(9).normal((F, Lv, D))
+    prompt = O.SeededRng(10).normal((Lt, D))
+    full = O.parallel_block_forward(blk, x, O.anchor_text(prompt, F), H)
+    fs = FrameSlices(blk, x, prompt, H, q_chunk=7)
+    for f in (2, 0, 3, 1, 2):
+        np.testing.assert_allclose(fs.step(f), full[f], atol=1e-12)
