@@ -25,6 +25,7 @@
 #include <math.h>
 
 #include "vc_attn_tc_common.cuh"
+#include "vc_tuning.h"
 
 namespace vc {
 
@@ -353,9 +354,16 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
   // kernel (vc_attn_tc3.cu); DP = 128: the one-tile kernel above.  Variants
   // measured slower in round 1 are in git history
   // (profiles/r01/attn_study/README.md).
+  // VC_ATTN_IMPL (tuning builds): 3 = the round-1 split-row kernel with half
+  // of P in shared memory; default 4 = P entirely in TMEM (vc_attn_tp.cu)
+  static const int impl = tuning_int("VC_ATTN_IMPL", 4);
   switch (DP) {
-    case 64: return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
-    case 80: return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 64:
+      if (impl == 3) return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_attn_tp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+    case 80:
+      if (impl == 3) return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+      return launch_attn_tp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 128: return launch_dp<128>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
   }
   set_error("tcgen05 attention: unsupported padded head dim %d", DP);

@@ -40,6 +40,11 @@ template <int DP>
 int launch_attn_tc3(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
                     int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
 
+// P-in-TMEM variant (112-key blocks; vc_attn_tp.cu), the default for DP <= 80.
+template <int DP>
+int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+                   int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st);
+
 // Padded head dim the tensor-core kernel uses for dh (0: unsupported).
 int attn_tc_head_pad(int dh);
 

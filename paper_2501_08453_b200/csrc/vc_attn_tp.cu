@@ -1,0 +1,411 @@
+// Flash attention with P entirely in TMEM ("tp"): two query tiles per CTA,
+// split-row softmax, key blocks of BK = 112 (DP 80) / 128 (DP 64).
+//
+// Same semantics and layouts as vc_attn_tc3.cu (numerics.py:87-107 per
+// (sequence, head); the full-sequence text keys deduplicated with + log2 F;
+// the ones column of V^T accumulating the row sum).  What changes is where P
+// lives.  In tc3 half of every P tile went through shared memory, and the
+// single P buffer made the exponentials of block j+1 wait for P.V of block j
+// (profiles/r01/attn_study: MUFU 60% busy, tensor pipe 49%, the period =
+// exp phase + P.V + handshakes).  Here, per 128-row tile, TMEM holds
+//     S [0, BK)   fp32 logits of the current key block
+//     P [BK, BK + BK/2)   bf16x2 probabilities (the A operand of a "ts" P.V)
+//     O [BK + BK/2, + DP) fp32 output accumulator (+ ones column)
+// which fits the tile's 256 columns because BK = 112: 112 + 56 + 80 = 248
+// (BK = 128 would need 272).  Consequences:
+//   * no P traffic on the shared-memory port and no generic->async proxy
+//     fence per block (tc3: P stores + P operand reads were ~40% of the
+//     port's wavefronts);
+//   * the softmax loads S(j+1), takes its max and exponentiates while
+//     P.V(j) still runs, and waits for P.V(j) only before overwriting P --
+//     in steady state P.V(j) finished long before (it is issued at the end
+//     of block j's exponentials), so the MUFU work of consecutive blocks is
+//     back to back.
+// The row max of the two warps sharing a row meets in shared memory.
+// 19 warps: w0 TMA, w1 / w2 MMA issuers of tile 0 / 1 (w1 owns TMEM),
+// w3..w18 softmax (w = 3 + 8*tile + 4*half + i; w % 4 is the TMEM lane
+// quarter).
+#include "vc_attn_tc_common.cuh"
+#include "vc_tuning.h"
+
+namespace vc {
+
+namespace {
+
+using namespace attn;
+
+#ifdef VC_ATTN_TRACE
+// clock64 phase stamps of one CTA (tools/attn_trace.cu): role 0 = MMA issuer,
+// 1 + sw = softmax warp sw (lane 0); j = key block (255: prologue/epilogue)
+__device__ unsigned long long g_attn_tracep[18][256][8];
+#define VC_TRP(cond, role, j, k)                                             \
+  do {                                                                       \
+    if ((cond) && (j) < 256) g_attn_tracep[role][j][k] = clock64();         \
+  } while (0)
+#else
+#define VC_TRP(cond, role, j, k) \
+  do {                           \
+  } while (0)
+#endif
+
+#ifdef VC_TP_SM_SPIN
+#define VC_SM_WAIT ptx::mbar_wait
+#else
+#define VC_SM_WAIT ptx::mbar_wait_sleep
+#endif
+
+constexpr int kWarpsTp = 19;
+constexpr int kThreadsTp = kWarpsTp * 32;
+
+template <int DP>
+struct CfgTp {
+  static constexpr int N64 = DP / 64;
+  static constexpr int TAIL = DP % 64;
+  static_assert(TAIL == 0 || TAIL == 16, "DP must be 64*n or 64*n+16");
+  static_assert(DP <= 80, "S + P + O must fit 256 TMEM columns per tile");
+  static constexpr int BK = DP == 64 ? 128 : 112;  // keys per block
+  static constexpr int HK = BK / 2;                // keys per softmax half
+  static constexpr int SCOL = 0, PCOL = BK, OCOL = BK + BK / 2;
+  static_assert(OCOL + DP <= 256, "per-tile TMEM columns");
+  static constexpr int Q_BYTES = BQ * DP * 2;
+  static constexpr int K_BYTES = BK * DP * 2;
+  static constexpr int K_STAGE = (K_BYTES + 1023) / 1024 * 1024;  // SW128 tiles start 1024-aligned
+  static constexpr int V_BYTES = DP * 128 * 2;  // two 64-key TMA boxes (keys past BK unused)
+  static constexpr int KS = 3;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KS * K_STAGE;
+  static constexpr int OFF_X = OFF_V + KS * V_BYTES;       // row-max exchange [2][2 tiles][2 halves][128]
+  static constexpr int OFF_BAR = OFF_X + 2 * 2 * 2 * BQ * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int KSTEPS = DP / 16;
+  static constexpr int NC = DP / 16;
+  static constexpr int NC0 = (NC + 1) / 2;
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+template <int DP, int POLY, bool ONES>
+__global__ void __launch_bounds__(kThreadsTp, 1)
+    attn_tp_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
+                   const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
+                   const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
+  using CF = CfgTp<DP>;
+  constexpr int KS = CF::KS, BK = CF::BK, HK = CF::HK;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;      // [KS]
+  uint64_t* k_empty = k_full + KS;  // [KS]
+  uint64_t* v_full = k_empty + KS;  // [KS]
+  uint64_t* v_empty = v_full + KS;  // [KS]
+  uint64_t* s_full = v_empty + KS;  // [2 tiles]
+  uint64_t* s_empty = s_full + 2;   // [2 tiles] S read into registers by both halves
+  uint64_t* p_full = s_empty + 2;   // [2 tiles] P written to TMEM
+  uint64_t* pv_done = p_full + 2;   // [2 tiles]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int q0 = blockIdx.x * (2 * BQ);
+  const int h = blockIdx.y;
+  const int seq = blockIdx.z;
+  const int n_tiles = (p.Lk + BK - 1) / BK;
+  const int ntile = q0 + BQ < p.Lq ? 2 : 1;  // the last CTA of a sequence may hold one tile
+  [[maybe_unused]] const bool tr = blockIdx.x == min(20u, gridDim.x - 1) && blockIdx.y == 3 && blockIdx.z == 0;
+
+  if (warp == 0 && ptx::elect_one()) {
+    ptx::prefetch_tmap(&tmQ64); ptx::prefetch_tmap(&tmK64); ptx::prefetch_tmap(&tmV);
+    if (CF::TAIL) { ptx::prefetch_tmap(&tmQ16); ptx::prefetch_tmap(&tmK16); }
+    ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < KS; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], ntile);  // one commit per tile issuer
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], ntile);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&s_empty[t], 256);
+      ptx::mbar_init(&p_full[t], 256);
+      ptx::mbar_init(&pv_done[t], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::fence_before_sync();
+  __syncthreads();
+  ptx::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (ptx::elect_one()) {
+      ptx::mbar_arrive_expect_tx(q_full, ntile * CF::Q_BYTES);
+      for (int t = 0; t < ntile; ++t) {
+        uint8_t* sQ = smem + CF::OFF_Q + t * CF::Q_BYTES;
+        for (int c = 0; c < CF::N64; ++c)
+          ptx::tma_load_4d(sQ + c * BQ * 128, &tmQ64, q_full, c * 64, h, q0 + t * BQ, seq);
+        if (CF::TAIL) ptx::tma_load_4d(sQ + CF::N64 * BQ * 128, &tmQ16, q_full, CF::N64 * 64, h, q0 + t * BQ, seq);
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % KS;
+        const uint32_t ph = ((j / KS) & 1) ^ 1;
+        const int k0 = j * BK;
+        ptx::mbar_wait_sleep(&k_empty[s], ph);
+        ptx::mbar_arrive_expect_tx(&k_full[s], CF::K_BYTES);
+        uint8_t* sK = smem + CF::OFF_K + s * CF::K_STAGE;
+        for (int c = 0; c < CF::N64; ++c)
+          ptx::tma_load_4d(sK + c * BK * 128, &tmK64, &k_full[s], c * 64, h, k0, seq);
+        if (CF::TAIL) ptx::tma_load_4d(sK + CF::N64 * BK * 128, &tmK16, &k_full[s], CF::N64 * 64, h, k0, seq);
+        ptx::mbar_wait_sleep(&v_empty[s], ph);
+        ptx::mbar_arrive_expect_tx(&v_full[s], CF::V_BYTES);
+        uint8_t* sV = smem + CF::OFF_V + s * CF::V_BYTES;
+        ptx::tma_load_4d(sV, &tmV, &v_full[s], k0, 0, h, seq);
+        ptx::tma_load_4d(sV + DP * 128, &tmV, &v_full[s], k0 + 64, 0, h, seq);
+      }
+    }
+  } else if (warp <= 2) {
+    // ===================== MMA issuers: warp 1 -> tile 0, warp 2 -> tile 1 =====================
+    // One issuer per query tile, so a tile's S(j+1) goes out the moment its
+    // softmax has read S(j) (s_empty) and its P.V(j) the moment P(j) is in
+    // TMEM, whatever the other tile is doing (a single in-order issuer tied
+    // each tile's next S to the other tile's P: the softmax waited ~500 clk
+    // per block for its logits, clock64 trace).  K / V stages are released
+    // when both tiles' MMAs have read them (k_empty / v_empty count ntile).
+    // Warp-uniform control flow, one elected lane issues; descriptors are
+    // bases + constant offsets in the start-address field (16-byte units).
+    const int t = warp - 1;
+    if (t < ntile) {
+      constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BK);
+      constexpr uint32_t idO = ptx::idesc_bf16_f32(BQ, DP);
+      const uint32_t sQ = ptx::smem_u32(smem + CF::OFF_Q + t * CF::Q_BYTES), sK = ptx::smem_u32(smem + CF::OFF_K),
+                     sV = ptx::smem_u32(smem + CF::OFF_V);
+      const uint64_t dQ = ptx::smem_desc(sQ, 0, 1024, ptx::kLayoutSW128);
+      const uint64_t dQt = ptx::smem_desc(sQ + CF::N64 * BQ * 128, 0, 256, ptx::kLayoutSW32);
+      const uint64_t dK = ptx::smem_desc(sK, 0, 1024, ptx::kLayoutSW128);
+      const uint64_t dKt = ptx::smem_desc(sK + CF::N64 * BK * 128, 0, 256, ptx::kLayoutSW32);
+      const uint64_t dV = ptx::smem_desc(sV, 0, 1024, ptx::kLayoutSW128);
+      const uint32_t tSd = tmem + t * 256 + CF::SCOL, tOd = tmem + t * 256 + CF::OCOL, tPa = tmem + t * 256 + CF::PCOL;
+      auto mma_s = [&](int ks) {  // S_t = Q_t K(ks)^T
+        const uint64_t ko = (uint64_t)((ks * CF::K_STAGE) >> 4);
+#pragma unroll
+        for (int c = 0; c < CF::KSTEPS; ++c) {
+          const bool tail = c >= 4 * CF::N64;
+          const uint64_t a = tail ? dQt : dQ + (uint64_t)(((c >> 2) * BQ * 128 + (c & 3) * 32) >> 4);
+          const uint64_t b = tail ? dKt + ko : dK + ko + (uint64_t)(((c >> 2) * BK * 128 + (c & 3) * 32) >> 4);
+          ptx::mma_bf16_ss(tSd, a, b, idS, c > 0);
+        }
+        ptx::mma_commit(&s_full[t]);
+        ptx::mma_commit(&k_empty[ks]);
+      };
+      auto mma_pv = [&](int ks, int j) {  // O_t += P_t V(ks)
+        const uint64_t vo = (uint64_t)((ks * CF::V_BYTES) >> 4);
+#pragma unroll
+        for (int c = 0; c < BK / 16; ++c)
+          ptx::mma_bf16_ts(tOd, tPa + 8 * c, dV + vo + (uint64_t)(((c >> 2) * DP * 128 + (c & 3) * 32) >> 4), idO,
+                           (j > 0 || c > 0) ? 1u : 0u);
+        ptx::mma_commit(&pv_done[t]);
+        ptx::mma_commit(&v_empty[ks]);
+      };
+      ptx::mbar_wait_sleep(q_full, 0);
+      ptx::mbar_wait_sleep(&k_full[0], 0);
+      ptx::fence_after_sync();
+      if (ptx::elect_one()) mma_s(0);
+      __syncwarp();
+      for (int j = 0; j < n_tiles; ++j) {
+        const int ks = j % KS;
+        VC_TRP(tr && (threadIdx.x & 31) == 0, t, j, 0);
+        if (j + 1 < n_tiles) {  // S(j+1) as soon as the softmax holds S(j) in registers
+          const int ks1 = (j + 1) % KS;
+          ptx::mbar_wait_sleep(&k_full[ks1], ((j + 1) / KS) & 1);
+          ptx::mbar_wait_sleep(&s_empty[t], j & 1);
+          ptx::fence_after_sync();
+          if (ptx::elect_one()) mma_s(ks1);
+          __syncwarp();
+        }
+        VC_TRP(tr && (threadIdx.x & 31) == 0, t, j, 1);
+        ptx::mbar_wait_sleep(&v_full[ks], (j / KS) & 1);
+        ptx::mbar_wait_sleep(&p_full[t], j & 1);
+        ptx::fence_after_sync();
+        if (ptx::elect_one()) mma_pv(ks, j);
+        __syncwarp();
+        VC_TRP(tr && (threadIdx.x & 31) == 0, t, j, 2);
+      }
+    }
+  } else {
+    // ===================== softmax (tile t, key half), correction, epilogue =====================
+    const int sw = warp - 3;
+    const int t = sw >> 3;
+    const int half = (sw >> 2) & 1;
+    const int quarter = warp & 3;
+    const int lane = threadIdx.x & 31;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + t * 256 + lane_off + CF::SCOL + half * HK;
+    const uint32_t tP = tmem + t * 256 + lane_off + CF::PCOL + half * (HK / 2);
+    const uint32_t tO = tmem + t * 256 + lane_off + CF::OCOL;
+    float* xs = reinterpret_cast<float*>(smem + CF::OFF_X);
+    const uint32_t bar_id = 1 + t * 4 + quarter;
+    const bool trs = tr && lane == 0;
+    if (t < ntile) {
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int kt = j * BK;
+        const int k0 = kt + half * HK;
+        const bool slow = kt < p.n_bias || kt + BK > p.Lk;  // tile-uniform: text keys / tail mask
+        VC_SM_WAIT(&s_full[t], j & 1);
+        ptx::fence_after_sync();
+        VC_TRP(trs, 2 + sw, j, 0);
+        uint32_t r[HK];
+        // one code path for both halves: pieces aligned for either start column
+        // (0 / HK = 56: 8-column pieces; 0 / 64: 32-column pieces)
+        // 32 / 16 / 8-column pieces (half 1 starts at column 56: the loads
+        // need no 32-column alignment; 7 x8 loads measured 2% slower)
+        ptx::tmem_ld_cols<0, HK>(tS, r);
+        ptx::tmem_ld_wait();
+        ptx::fence_before_sync();
+        ptx::mbar_arrive(&s_empty[t]);  // S lives in registers now
+        if (slow) {
+#pragma unroll
+          for (int i = 0; i < HK; ++i) {
+            float x = __uint_as_float(r[i]) * p.scale_log2;
+            if (k0 + i < p.n_bias) x += p.bias_log2;
+            if (k0 + i >= p.Lk) x = -INFINITY;
+            r[i] = __float_as_uint(x);
+          }
+        }
+        // row max of this half: four FMNMX3 chains (two logits per instruction)
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int i = 0; i < HK; i += 2)
+          m4[(i >> 1) & 3] = ptx::fmax3(m4[(i >> 1) & 3], __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+        float pm = ptx::fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+        if (!slow) pm *= p.scale_log2;
+        // the two halves' partial maxima meet in shared memory (parity-buffered)
+        float* xj = xs + ((j & 1) * 4 + t * 2) * BQ;
+        xj[half * BQ + row] = pm;
+        ptx::named_bar_sync(bar_id, 64);
+        const float mx = fmaxf(pm, xj[(half ^ 1) * BQ + row]);
+        VC_TRP(trs, 2 + sw, j, 1);
+        float alpha = 1.f;
+        if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
+          alpha = ptx::ex2(m_used - mx);         // 0 on the first block
+          m_used = mx;
+        }
+        const float sc = slow ? 1.f : p.scale_log2;
+        const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m_used, -m_used);
+        float2 s2 = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
+        uint32_t pk[HK / 2];
+#pragma unroll
+        for (int i = 0; i < HK; i += 2) {
+          float2 e = ptx::ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nm2);
+          if (POLY > 0 && ((i >> 1) % (POLY > 0 ? POLY : 1)) == POLY - 1) {
+            e = ptx::ex2_poly2(e);
+          } else {
+            e.x = ptx::ex2(e.x);
+            e.y = ptx::ex2(e.y);
+          }
+          if (!ONES) {
+            if (i & 2) s2b = ptx::fadd2(s2b, e); else s2 = ptx::fadd2(s2, e);
+          }
+          pk[i >> 1] = ptx::bf16x2(e.x, e.y);
+        }
+        if (!ONES) {
+          s2 = ptx::fadd2(s2, s2b);
+          l = l * alpha + (s2.x + s2.y);  // this half's partial row sum
+        }
+        VC_TRP(trs, 2 + sw, j, 2);
+        if (j > 0) {  // P.V(j-1) must be done reading P (and adding into O) before P and O change
+          VC_SM_WAIT(&pv_done[t], (j - 1) & 1);
+          ptx::fence_after_sync();
+        }
+        VC_TRP(trs, 2 + sw, j, 3);
+#ifdef VC_TP_ST_NARROW
+#pragma unroll
+        for (int c = 0; c < HK / 2; c += 4) ptx::tmem_st4p(tP + c, pk + c);
+#else
+        ptx::tmem_st_cols<0, HK / 2>(tP, pk);
+#endif
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          if (half == 0) rescale_o<DP, 0, CF::NC0>(tO, alpha);
+          else rescale_o<DP, CF::NC0, CF::NC>(tO, alpha);
+        }
+        ptx::tmem_st_wait();
+        ptx::fence_before_sync();
+        ptx::mbar_arrive(&p_full[t]);
+        VC_TRP(trs, 2 + sw, j, 4);
+      }
+      VC_SM_WAIT(&pv_done[t], (n_tiles - 1) & 1);
+      ptx::fence_after_sync();
+      if (ONES) {  // row sum accumulated by the tensor core in the ones column
+        uint32_t r1;
+        ptx::tmem_ld1(tO + p.dh, r1);
+        ptx::tmem_ld_wait();
+        l = __uint_as_float(r1);
+      } else {  // the two halves' partial sums (same alpha history) add up
+        float* xj = xs + ((n_tiles & 1) * 4 + t * 2) * BQ;
+        xj[half * BQ + row] = l;
+        ptx::named_bar_sync(bar_id, 64);
+        l += xj[(half ^ 1) * BQ + row];
+      }
+      if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
+      else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
+    }
+  }
+  ptx::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::fence_after_sync();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+#ifdef VC_ATTN_TRACE
+int attn_tracep_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_attn_tracep, sizeof(g_attn_tracep)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
+template <int DP>
+int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+                   int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
+  using CF = CfgTp<DP>;
+  AttnMaps m;
+  VC_TRY((make_attn_maps<DP, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
+  const bool ones = p.dh < DP;
+  static const int poly = tuning_int("VC_POLY_EVERY", 4);
+  dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
+#define VC_ATTN_TP_CASE(PV, ON)                                                                                  \
+  if (poly == PV && ones == ON) {                                                                               \
+    static bool attr = false;                                                                                   \
+    if (!attr) {                                                                                                \
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, PV, ON>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         CF::SMEM));                                                            \
+      attr = true;                                                                                              \
+    }                                                                                                           \
+    attn_tp_kernel<DP, PV, ON><<<grid, kThreadsTp, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);         \
+    VC_CHECK_LAUNCH();                                                                                          \
+    return VC_OK;                                                                                               \
+  }
+  VC_ATTN_TP_CASE(4, true)
+  VC_ATTN_TP_CASE(4, false)
+#ifdef VC_TUNING
+  VC_ATTN_TP_CASE(2, true)
+  VC_ATTN_TP_CASE(3, true)
+  VC_ATTN_TP_CASE(6, true)
+  VC_ATTN_TP_CASE(8, true)
+  VC_ATTN_TP_CASE(0, true)
+#endif
+#undef VC_ATTN_TP_CASE
+  set_error("attention variant not built (tuning builds: VC_POLY_EVERY 0, 2, 3, 4)");
+  return VC_EINVAL;
+}
+
+template int launch_attn_tp<64>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t, int64_t,
+                                int64_t, cudaStream_t);
+template int launch_attn_tp<80>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t, int64_t,
+                                int64_t, cudaStream_t);
+
+}  // namespace vc

@@ -48,6 +48,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Same, but a thread whose phase is not complete is suspended (up to the
+// hint, in ns) until the barrier completes instead of spinning: a polling
+// warp costs the issue slots of the warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+
 // ---- TMA ---------------------------------------------------------------------
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -295,6 +310,64 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
       "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
+__device__ __forceinline__ void tmem_ld8p(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8p(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+}
+__device__ __forceinline__ void tmem_st4p(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]));
+}
+__device__ __forceinline__ void tmem_ld4p(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+// Columns [C, C + N) of an aligned TMEM region (base) <-> r[0..N), in pieces
+// of 32 / 16 / 8 / 4 columns each starting at a multiple of its own width.
+template <int C, int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t base, uint32_t* r) {
+  if constexpr (N >= 32 && C % 32 == 0) {
+    tmem_ld32(base + C, *reinterpret_cast<uint32_t(*)[32]>(r));
+    tmem_ld_cols<C + 32, N - 32>(base, r + 32);
+  } else if constexpr (N >= 16 && C % 16 == 0) {
+    tmem_ld16p(base + C, r);
+    tmem_ld_cols<C + 16, N - 16>(base, r + 16);
+  } else if constexpr (N >= 8 && C % 8 == 0) {
+    tmem_ld8p(base + C, r);
+    tmem_ld_cols<C + 8, N - 8>(base, r + 8);
+  } else if constexpr (N >= 4) {
+    static_assert(C % 4 == 0, "tmem_ld_cols: 4-column granularity");
+    tmem_ld4p(base + C, r);
+    tmem_ld_cols<C + 4, N - 4>(base, r + 4);
+  } else {
+    static_assert(N == 0, "tmem_ld_cols: N multiple of 4");
+  }
+}
+template <int C, int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t base, const uint32_t* r) {
+  if constexpr (N >= 32 && C % 32 == 0) {
+    tmem_st32(base + C, *reinterpret_cast<const uint32_t(*)[32]>(r));
+    tmem_st_cols<C + 32, N - 32>(base, r + 32);
+  } else if constexpr (N >= 16 && C % 16 == 0) {
+    tmem_st16(base + C, *reinterpret_cast<const uint32_t(*)[16]>(r));
+    tmem_st_cols<C + 16, N - 16>(base, r + 16);
+  } else if constexpr (N >= 8 && C % 8 == 0) {
+    tmem_st8p(base + C, r);
+    tmem_st_cols<C + 8, N - 8>(base, r + 8);
+  } else if constexpr (N >= 4) {
+    static_assert(C % 4 == 0, "tmem_st_cols: 4-column granularity");
+    tmem_st4p(base + C, r);
+    tmem_st_cols<C + 4, N - 4>(base, r + 4);
+  } else {
+    static_assert(N == 0, "tmem_st_cols: N multiple of 4");
+  }
+}
 __device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r));
 }
@@ -303,6 +376,13 @@ __device__ __forceinline__ void tmem_ld_wait() {
 }
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// max(a, b, c) in one FMNMX3 (sm_100)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
 }
 
 // 2^x on the MUFU pipe (ex2.approx.ftz: one SASS MUFU.EX2, ~2 ulp; -inf -> +0)

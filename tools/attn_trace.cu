@@ -15,6 +15,7 @@
 
 namespace vc {
 int attn_trace3_read(unsigned long long* host);
+int attn_tracep_read(unsigned long long* host);
 }
 
 __global__ void fill_kernel(__nv_bfloat16* x, size_t n, uint32_t seed, float amp) {
@@ -61,10 +62,11 @@ int main(int argc, char** argv) {
   const double flop = 4.0 * Lq * (double)Lk * H * dh;
   printf("# Lq %d Lk %d H %d dh %d DP %d: %.4f ms  %.1f TFLOP/s (algorithmic dh)\n", Lq, Lk, H, dh, DP, ms,
          flop / ms / 1e9);
-  const int nroles = 17;
   const int nj = 256;
-  std::vector<unsigned long long> tr(17 * 512 * 8);
-  const int trc = vc::attn_trace3_read(tr.data());
+  std::vector<unsigned long long> tr(18 * 512 * 8);
+  const char* impl = getenv("VC_ATTN_IMPL");
+  const int nroles = (impl && atoi(impl) == 3) ? 17 : 18;
+  const int trc = (impl && atoi(impl) == 3) ? vc::attn_trace3_read(tr.data()) : vc::attn_tracep_read(tr.data());
   if (trc == 0) {
     unsigned long long t0 = ~0ull;
     for (auto v : tr) if (v && v < t0) t0 = v;
