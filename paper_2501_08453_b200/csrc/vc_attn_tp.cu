@@ -257,8 +257,6 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
         ptx::fence_after_sync();
         VC_TRP(trs, 2 + sw, j, 0);
         uint32_t r[HK];
-        // one code path for both halves: pieces aligned for either start column
-        // (0 / HK = 56: 8-column pieces; 0 / 64: 32-column pieces)
         // 32 / 16 / 8-column pieces (half 1 starts at column 56: the loads
         // need no 32-column alignment; 7 x8 loads measured 2% slower)
         ptx::tmem_ld_cols<0, HK>(tS, r);
@@ -320,12 +318,7 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
           ptx::fence_after_sync();
         }
         VC_TRP(trs, 2 + sw, j, 3);
-#ifdef VC_TP_ST_NARROW
-#pragma unroll
-        for (int c = 0; c < HK / 2; c += 4) ptx::tmem_st4p(tP + c, pk + c);
-#else
-        ptx::tmem_st_cols<0, HK / 2>(tP, pk);
-#endif
+        ptx::tmem_st_cols<0, HK / 2>(tP, pk);  // 16 / 8 / 4-column pieces (x4 only: 2% slower)
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           if (half == 0) rescale_o<DP, 0, CF::NC0>(tO, alpha);
           else rescale_o<DP, CF::NC0, CF::NC>(tO, alpha);

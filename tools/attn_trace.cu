@@ -66,7 +66,8 @@ int main(int argc, char** argv) {
   std::vector<unsigned long long> tr(18 * 512 * 8);
   const char* impl = getenv("VC_ATTN_IMPL");
   const int nroles = (impl && atoi(impl) == 3) ? 17 : 18;
-  const int trc = (impl && atoi(impl) == 3) ? vc::attn_trace3_read(tr.data()) : vc::attn_tracep_read(tr.data());
+  const int iv = impl ? atoi(impl) : 4;
+  const int trc = iv == 3 ? vc::attn_trace3_read(tr.data()) : vc::attn_tracep_read(tr.data());
   if (trc == 0) {
     unsigned long long t0 = ~0ull;
     for (auto v : tr) if (v && v < t0) t0 = v;
