@@ -197,6 +197,13 @@ VC_API int vc_gemm_bf16(const void* a_dev, int64_t lda, const void* b_dev,
                         const float* resid_dev, float* out_dev, int64_t ldo,
                         int64_t M, int32_t N, int32_t K, void* stream);
 
+/* Temporal-branch kernel choice for the bf16 block (test / profiling aid):
+ * 0 the measured rule (default: the tcgen05 + TMA kernel on 64..128-frame,
+ * dh >= 128 sequences, the mma.sync kernel elsewhere), 1 mma.sync, 2 the
+ * tcgen05 + TMA kernel wherever it applies (F <= 176, dh <= 128).
+ * Process-wide; not thread-safe against concurrent forwards. */
+VC_API int vc_set_temporal_impl(int32_t impl);
+
 /* ---- Sequence parallelism (the paper's hybrid-parallel scheme) ----------
  * Spatial shard axis, head-parallel (Ulysses) attention, separate text
  * placement: executor.py:561-626 (run_sp_iteration stage 3) with the two

@@ -49,7 +49,7 @@ template <int KS, int NT, bool VEC16>
 __global__ void __launch_bounds__(kWarps * 32)
     temporal_mma_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int64_t D,
                         __nv_bfloat16* __restrict__ o, int64_t ldo, int F, int Lv, int H, int dh,
-                        float scale_log2, int hs) {
+                        float scale_log2, int hs, int pos_major) {
   constexpr int KPAD = 16 * KS + 8;  // smem row pitch (elements): conflict-free ldmatrix
   __shared__ __align__(16) __nv_bfloat16 sK[kWarps][16][KPAD];
   __shared__ __align__(16) __nv_bfloat16 sV[kWarps][16][KPAD];
@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(kWarps * 32)
   uint32_t qa[KS][4];
   {
     const int fr0 = f0 + g, fr1 = f0 + g + 8;
-    const __nv_bfloat16* r0 = qkv + ((int64_t)fr0 * Lv + l) * ld + col0;
-    const __nv_bfloat16* r1 = qkv + ((int64_t)fr1 * Lv + l) * ld + col0;
+    const __nv_bfloat16* r0 = qkv + (pos_major ? (int64_t)l * F + fr0 : (int64_t)fr0 * Lv + l) * ld + col0;
+    const __nv_bfloat16* r1 = qkv + (pos_major ? (int64_t)l * F + fr1 : (int64_t)fr1 * Lv + l) * ld + col0;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int c0 = ks * 16 + 2 * t, c1 = c0 + 8;
@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int r = e / CH, c = (e - r * CH) * 8;
         const int fr = k0 + r;
         const bool ok = fr < F && c < dh;
-        const __nv_bfloat16* row = qkv + ((int64_t)(ok ? fr : 0) * Lv + l) * ld + col0 + (ok ? c : 0);
+        const int64_t rr0 = pos_major ? (int64_t)l * F + (ok ? fr : 0) : (int64_t)(ok ? fr : 0) * Lv + l;
+        const __nv_bfloat16* row = qkv + rr0 * ld + col0 + (ok ? c : 0);
         cp_async16(ptx::smem_u32(&sK[warp][r][c]), row + D, ok);
         cp_async16(ptx::smem_u32(&sV[warp][r][c]), row + 2 * D, ok);
       }
@@ -106,7 +107,8 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int r = e / words, c = 2 * (e - r * words);
         const int fr = k0 + r;
         const bool ok = fr < F && c < dh;
-        const __nv_bfloat16* row = qkv + ((int64_t)(ok ? fr : 0) * Lv + l) * ld + col0 + (ok ? c : 0);
+        const int64_t rr0 = pos_major ? (int64_t)l * F + (ok ? fr : 0) : (int64_t)(ok ? fr : 0) * Lv + l;
+        const __nv_bfloat16* row = qkv + rr0 * ld + col0 + (ok ? c : 0);
         cp_async4(ptx::smem_u32(&sK[warp][r][c]), row + D, ok);
         cp_async4(ptx::smem_u32(&sV[warp][r][c]), row + 2 * D, ok);
       }
@@ -241,16 +243,16 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 template <int KS, int NT>
 int launch_ks(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo, int F, int Lv,
-              int H, int dh, cudaStream_t st, int hs) {
+              int H, int dh, cudaStream_t st, int hs, int pm) {
   const int64_t items = (int64_t)Lv * H * ((F + 15) / 16);
   const int64_t blocks = cdiv(items, kWarps);
   if (blocks > 2147483647) { set_error("temporal grid too large"); return VC_ENOTSUP; }
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)dh));
   const bool vec16 = dh % 8 == 0 && ld % 8 == 0 && D % 8 == 0 && ((uintptr_t)qkv % 16) == 0;
   if (vec16)
-    temporal_mma_kernel<KS, NT, true><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs);
+    temporal_mma_kernel<KS, NT, true><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs, pm);
   else
-    temporal_mma_kernel<KS, NT, false><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs);
+    temporal_mma_kernel<KS, NT, false><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs, pm);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
@@ -258,7 +260,7 @@ int launch_ks(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o,
 }  // namespace
 
 int launch_temporal_mma(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo, int F,
-                        int Lv, int H, int dh, cudaStream_t st, int head_slot) {
+                        int Lv, int H, int dh, cudaStream_t st, int head_slot, int pos_major) {
   if (F <= 0 || Lv <= 0) return VC_OK;
   const int hs = head_slot ? head_slot : dh;
   if (hs < dh || (head_slot && head_slot > 16 * ((dh + 15) / 16))) {
@@ -271,14 +273,14 @@ int launch_temporal_mma(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bf
   }
   const int ks = (dh + 15) / 16;
   switch (ks) {
-    case 1: return launch_ks<1, 2>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
-    case 2: return launch_ks<2, 4>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
-    case 3: return launch_ks<3, 6>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
-    case 4: return launch_ks<4, 8>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
-    case 5: return launch_ks<5, 10>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
-    case 6: return launch_ks<6, 12>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
-    case 7: return launch_ks<7, 14>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
-    default: return launch_ks<8, 16>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs);
+    case 1: return launch_ks<1, 2>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
+    case 2: return launch_ks<2, 4>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
+    case 3: return launch_ks<3, 6>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
+    case 4: return launch_ks<4, 8>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
+    case 5: return launch_ks<5, 10>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
+    case 6: return launch_ks<6, 12>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
+    case 7: return launch_ks<7, 14>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
+    default: return launch_ks<8, 16>(qkv, ld, D, o, ldo, F, Lv, H, dh, st, hs, pos_major);
   }
 }
 

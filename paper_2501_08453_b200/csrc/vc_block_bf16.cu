@@ -85,6 +85,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   sc.sp = BranchOut{(bf*)(ws + wl.qsp), (bf*)(ws + wl.ksp), (bf*)(ws + wl.vtsp), wl.Lv_ld};
   sc.fs = BranchOut{(bf*)(ws + wl.qfs), (bf*)(ws + wl.kfs), (bf*)(ws + wl.vtfs), wl.Lk_ld};
   sc.tm = tm;
+  sc.tm_F = (int)F;  // temporal q/k/v position-major: each position's F frames are consecutive rows
   const int qkv_epi = ext ? EPI_QKVN : EPI_QKV;
   if (ext) {
     sc.qn[0] = ext->qn[0]; sc.qn[1] = ext->qn[1]; sc.kn[0] = ext->kn[0]; sc.kn[1] = ext->kn[1];
@@ -136,7 +137,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_attn_tc(a, sc.sp.q, sc.sp.k, sc.sp.vt, (int)F, Lv, Lv, wl.Lv_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_spatial");
-  VC_TRY(launch_temporal_mma(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, st, slot));
+  VC_TRY(launch_temporal_bf16(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, st, slot, 1));
   profile_mark(st, "attn_temporal");
   {
     AttnTcParams a{};

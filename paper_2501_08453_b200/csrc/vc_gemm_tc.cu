@@ -148,7 +148,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
     const int64_t n = n0 + s.n_base;
     if (n >= 3 * q.SEG && n < q.fs_base()) {  // temporal: plain [row][3D]
       const int64_t j = n - 3 * q.SEG;
-      __nv_bfloat16* o = s.tm + m * 3 * s.D + j;
+      int64_t row = m;
+      if (s.tm_F) {  // position-major: row l*F + f
+        const int fr = sp_f >= 0 ? sp_f : qkv_frame(s, m);
+        row = (m - (int64_t)fr * s.Lv) * s.tm_F + fr;
+      }
+      __nv_bfloat16* o = s.tm + row * 3 * s.D + j;
       if (j + 16 <= 3 * s.D && n0 + 16 <= p.N) {
         uint4 a, b;
         a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);

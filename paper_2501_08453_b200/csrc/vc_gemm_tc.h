@@ -32,6 +32,10 @@ struct QkvScatter {
   int32_t text_rows;  // rows are prompt rows (full-sequence keys 0..Lt-1)
   BranchOut sp, fs;
   __nv_bfloat16* tm;  // temporal branch, plain [row][3D]
+  // 0: tm rows in GEMM row order (frame-major f*Lv + l); F > 0: position-major
+  // rows l*F + f, so a position's F frames are consecutive rows (the
+  // temporal attention's sequences, read as whole boxes)
+  int32_t tm_F;
   // mode 1 (sequence-parallel send): spatial / full-seq Q, K, V of local row m
   // and head h go to send[b'][g][which][m][h % Hg][DP], g = h / Hg (head group
   // owner), b' = 0 spatial / 1 full sequence (branch-major, so each branch's

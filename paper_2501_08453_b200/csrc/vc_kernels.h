@@ -24,8 +24,16 @@ int launch_temporal_attn(const T* qkv, int64_t ld, int64_t D, OutT* o, int64_t l
                          int H, int dh, cudaStream_t st);
 
 // bf16 temporal branch on warp-level tensor-core MMAs (vc_attn_temporal_mma.cu)
+// pos_major: q/k/v row of (frame f, position l) is l*F + f (else f*Lv + l)
 int launch_temporal_mma(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo,
-                        int F, int Lv, int H, int dh, cudaStream_t st, int head_slot = 0);
+                        int F, int Lv, int H, int dh, cudaStream_t st, int head_slot = 0, int pos_major = 0);
+// bf16 temporal branch on tcgen05 + TMA (vc_attn_temporal_tc.cu), F <= 176, dh <= 128
+bool temporal_tc_supported(int64_t ld, int64_t D, int F, int dh, const void* qkv);
+int launch_temporal_tc(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo, int F,
+                       int Lv, int H, int dh, cudaStream_t st, int head_slot = 0, int pos_major = 0);
+// the bf16 temporal branch: tcgen05 kernel where it applies, else the mma.sync one
+int launch_temporal_bf16(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo, int F,
+                         int Lv, int H, int dh, cudaStream_t st, int head_slot = 0, int pos_major = 0);
 
 template <typename OutT>
 int launch_ln_rows(const float* x, int64_t n_x, const float* p, int64_t n_p, int D, OutT* out,

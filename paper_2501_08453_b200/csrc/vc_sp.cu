@@ -449,7 +449,7 @@ int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loca
     VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
     profile_mark(st, "sp_qkv_gemm");
     // temporal branch is rank-local: sequence = local position, tokens = frames (stride vc)
-    VC_TRY(launch_temporal_mma(tm, 3 * x.D, x.D, acat + x.BW, 3 * x.BW, (int)x.F, vc, (int)x.H, (int)x.dh, st,
+    VC_TRY(launch_temporal_bf16(tm, 3 * x.D, x.D, acat + x.BW, 3 * x.BW, (int)x.F, vc, (int)x.H, (int)x.dh, st,
                                (int)x.S));
     profile_mark(st, "sp_attn_temporal");
   }
@@ -601,7 +601,7 @@ int vc_spg_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loc
     s.fs = BranchOut{(bf*)(W + w.qfs), slot + gs.C, slot + gs.Dv, gs.fsl_ld};
     VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
     profile_mark(st, "spg_qkv_gemm");
-    VC_TRY(launch_temporal_mma(tm, 3 * x.D, x.D, acat + x.D, 3 * x.D, (int)x.F, vc, (int)x.H, (int)x.dh, st));
+    VC_TRY(launch_temporal_bf16(tm, 3 * x.D, x.D, acat + x.D, 3 * x.D, (int)x.F, vc, (int)x.H, (int)x.dh, st));
     profile_mark(st, "spg_attn_temporal");
   }
   if (x.Lt > 0) {  // text K, V of all heads from the local prompt copy -> global full-seq keys [0, Lt)
