@@ -248,6 +248,12 @@ VC_API int vc_sp_stage1(const vc_sp_plan* plan, const void* packed_dev,
                         const float* x_local_dev, const float* prompt_dev,
                         void* send1_dev, void* workspace_dev,
                         size_t workspace_bytes, void* stream);
+/* vc_sp_stage1 in two parts, so the host can start a2a #1 after the QKV GEMM
+ * and run the rank-local temporal branch under it: part 0 = LN + QKV GEMM
+ * (fills send1), 1 = temporal branch, 2 = both (= vc_sp_stage1). */
+VC_API int vc_sp_stage1_part(const vc_sp_plan* plan, const void* packed_dev, const float* x_local,
+                             const float* prompt, void* send1, int32_t part, void* workspace,
+                             size_t workspace_bytes, void* stream);
 /* One branch of stage 2 (0 spatial, 1 full sequence): that branch's half of
  * recv1 -> head-group attention -> that branch's half of send2. */
 VC_API int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed_dev,

@@ -439,6 +439,34 @@ def fullseq_global_order(frames, text_len, visual_len, p):
     return idx_by_dev, order
 
 
+def comm_plan(frames, text_len, visual_len, dim, heads, depth, p, attention="head_parallel", bpe=8,
+              placement="intra"):
+    """executor.py:721-773 -- the collective schedule run_sp_iteration logs
+    (spatial shard axis, separate text placement, one node): rows of
+    (stage, collective, group_size, placement, bytes_per_device)
+    (CommEvent.key, executor.py:100-108). Pinned by the reference
+    executor's own log (tests/golden sp_p{P}_comm)."""
+    if p <= 1:
+        return []
+    tcounts, vcounts = placement_division(text_len, visual_len, p, "separate")
+    fsizes = [len(fs) for fs in round_robin_frames(frames, p)]
+    col_width = dim // p if attention == "head_parallel" else dim
+    rows = [("reshard", "alltoall", p, placement, float(max(fsizes) * visual_len * dim * bpe))]
+
+    def branch(stage, rows_per_dev, needed_rows):
+        if attention == "head_parallel":
+            rows.append((stage, "alltoall", p, placement, float(3 * max(rows_per_dev) * dim * bpe)))
+            rows.append((stage, "alltoall", p, placement, float(needed_rows * col_width * bpe)))
+        else:
+            rows.append((stage, "allgather", p, placement, float(2 * max(rows_per_dev) * dim * bpe)))
+
+    for bi in range(depth):
+        branch(f"block{bi}.spatial", [frames * v for v in vcounts], frames * visual_len)
+        branch(f"block{bi}.fullseq", [frames * (t + v) for t, v in zip(tcounts, vcounts)], frames * visual_len)
+    rows.append(("gather", "allgather", p, placement, float(max(frames * v for v in vcounts) * dim * bpe)))
+    return rows
+
+
 def head_parallel_block(block, visual, text, heads, p):
     """executor.py:561-626 stage 3 (spatial axis, head-parallel, separate
     text placement) for one block, simulated on p logical devices in one

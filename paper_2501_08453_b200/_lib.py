@@ -68,6 +68,7 @@ SIGNATURES = {
     "vc_sp_row_map": (_i32, [C.POINTER(SpPlan), _i32, C.c_void_p]),
     "vc_set_temporal_impl": (C.c_int, [_i32]),
     "vc_sp_stage1": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _p, _sz, _p]),
+    "vc_sp_stage1_part": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _i32, _p, _sz, _p]),
     "vc_sp_stage2": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, _sz, _p]),
     "vc_sp_stage2_branch": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _i32, _p, _sz, _p]),
     "vc_sp_stage3": (C.c_int, [C.POINTER(SpPlan), _p, _p, _p, _p, C.c_int, _p, _sz, _p]),

@@ -425,6 +425,12 @@ int vc_sp_row_map(const vc_sp_plan* plan, int32_t which, int64_t* out) {
 
 int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_local, const float* prompt,
                  void* send1, void* ws, size_t ws_bytes, void* stream) {
+  return vc_sp_stage1_part(plan, packed, x_local, prompt, send1, 2, ws, ws_bytes, stream);
+}
+
+int vc_sp_stage1_part(const vc_sp_plan* plan, const void* packed, const float* x_local, const float* prompt,
+                      void* send1, int32_t part, void* ws, size_t ws_bytes, void* stream) {
+  if (part < 0 || part > 2) { set_error("stage-1 part must be 0 (LN + QKV GEMM), 1 (temporal) or 2 (both)"); return VC_EINVAL; }
   Sp x;
   VC_TRY(sp_make(plan, &x));
   const SpWs w = sp_ws(x);
@@ -438,9 +444,11 @@ int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loca
   bf* xhat = (bf*)(W + w.xhat);
   bf* tm = (bf*)(W + w.tm);
   bf* acat = (bf*)(W + w.acat);
-  VC_TRY(launch_ln_rows<bf>(x_local, Mr, prompt, x.Lt, (int)x.D, xhat, st));
-  profile_mark(st, "sp_ln");
-  if (Mr > 0) {
+  if (part != 1) {
+    VC_TRY(launch_ln_rows<bf>(x_local, Mr, prompt, x.Lt, (int)x.D, xhat, st));
+    profile_mark(st, "sp_ln");
+  }
+  if (Mr > 0 && part != 1) {
     GemmTcParams g{};
     g.M = Mr; g.N = (int)x.pad.Npad; g.K = (int)x.D; g.bias = pp.bias;
     QkvScatter& s = g.qkv;
@@ -448,6 +456,8 @@ int vc_sp_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loca
     s.mode = 1; s.Hg = (int)x.Hg; s.send_rows = Mr; s.send = (bf*)send1;
     VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
     profile_mark(st, "sp_qkv_gemm");
+  }
+  if (Mr > 0 && part != 0) {
     // temporal branch is rank-local: sequence = local position, tokens = frames (stride vc)
     VC_TRY(launch_temporal_bf16(tm, 3 * x.D, x.D, acat + x.BW, 3 * x.BW, (int)x.F, vc, (int)x.H, (int)x.dh, st,
                                (int)x.S));

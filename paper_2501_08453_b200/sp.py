@@ -18,6 +18,7 @@ and (b) P virtual ranks in one process on one GPU for the parity test.
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -129,6 +130,58 @@ class TorchExchange:
         self.dist.all_gather_into_tensor(gather, gather[rank * n:(rank + 1) * n], group=self.group)
 
 
+@dataclass(frozen=True)
+class CommEvent:
+    """One collective this rank issued (executor.py:91-108's CommEvent fields;
+    bytes_per_device is what this rank hands to the collective, its own
+    block included, as laid out; payload_bytes the same exchange without
+    the layout padding, in the reference's payload terms)."""
+    stage: str
+    collective: str
+    group_size: int
+    placement: str
+    bytes_per_device: float
+    payload_bytes: float = 0.0
+
+    def key(self) -> tuple:
+        return (self.stage, self.collective, self.group_size, self.placement, self.bytes_per_device)
+
+
+@dataclass
+class CommLog:
+    """Ordered record of the collectives one forward issued (executor.py:111-141)."""
+    events: list = field(default_factory=list)
+
+    def record(self, stage, collective, group_size, placement, bytes_per_device, payload_bytes=0.0):
+        self.events.append(CommEvent(stage, collective, int(group_size), placement, float(bytes_per_device),
+                                     float(payload_bytes)))
+
+    def rows(self) -> list:
+        return [e.key() for e in self.events]
+
+
+class LoggedExchange:
+    """Wraps an exchange (TorchExchange: NCCL on the GPU box, gloo in the CPU
+    tests) and records every collective run_stages / sp_model_forward issue
+    into a CommLog, with the bytes actually handed to the collective."""
+
+    def __init__(self, inner, log: CommLog, group_size: int, bpe: int = 2, placement: str = "intra"):
+        self.inner, self.log, self.P, self.bpe, self.placement = inner, log, group_size, bpe, placement
+        self.stage = "?"
+        self.payload = None  # reference-payload element count of the next exchange (set by the driver)
+
+    def all_to_all(self, recv, send, recv_counts, send_counts, async_op=False):
+        self.log.record(self.stage, "alltoall", self.P, self.placement, sum(send_counts) * self.bpe,
+                        (self.payload if self.payload is not None else sum(send_counts)) * self.bpe)
+        self.payload = None
+        return self.inner.all_to_all(recv, send, recv_counts, send_counts, async_op=async_op)
+
+    def all_gather(self, gather, rank):
+        n = gather.numel() // self.P
+        self.log.record(self.stage, "allgather", self.P, self.placement, n * self.bpe, n * self.bpe)
+        return self.inner.all_gather(gather, rank)
+
+
 # ---------------------------------------------------------------------------
 # The rank-local CUDA stages
 # ---------------------------------------------------------------------------
@@ -159,6 +212,8 @@ class SPBlock:
         self.vb = list(vb)
         self.counts = {k: [int(lib.vc_sp_exchange_elems(C.byref(self.plan), i, r)) for r in range(nranks)]
                        for i, k in enumerate(("send1", "recv1", "send2", "recv2"))}
+        self.payload_counts = {k: [int(lib.vc_sp_exchange_elems(C.byref(self.plan), 4 + i, r)) for r in range(nranks)]
+                               for i, k in enumerate(("send1", "recv1", "send2", "recv2"))}
         dev = "cuda"
         bf = torch.bfloat16
         self.send1 = torch.empty(sum(self.counts["send1"]), dtype=bf, device=dev)
@@ -172,11 +227,13 @@ class SPBlock:
     def local_rows(self):
         return self.vb[self.rank], self.vb[self.rank + 1]
 
-    def stage1(self, x_local, prompt):
+    def stage1(self, x_local, prompt, part=2):
+        """part 0: LN + QKV GEMM (fills send1), 1: temporal branch, 2: both."""
         lib = _lib.load()
-        _lib.check(lib.vc_sp_stage1(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(x_local),
-                                    _lib.ptr(prompt) if self.Lt else C.c_void_p(0), _lib.ptr(self.send1),
-                                    _lib.ptr(self.ws), self.ws_bytes, _lib.stream_ptr(self.torch)), "sp stage1")
+        _lib.check(lib.vc_sp_stage1_part(C.byref(self.plan), _lib.ptr(self.db.packed), _lib.ptr(x_local),
+                                         _lib.ptr(prompt) if self.Lt else C.c_void_p(0), _lib.ptr(self.send1),
+                                         int(part), _lib.ptr(self.ws), self.ws_bytes,
+                                         _lib.stream_ptr(self.torch)), "sp stage1")
 
     def stage2(self, branch=None):
         """Both branches, or one (0 spatial / 1 full sequence)."""
@@ -196,10 +253,10 @@ class SPBlock:
                                     _lib.ptr(x_local), _lib.ptr(out_local), 1 if add_residual else 0,
                                     _lib.ptr(self.ws), self.ws_bytes, _lib.stream_ptr(self.torch)), "sp stage3")
 
-    def forward(self, x_local, prompt, out_local, exchange, add_residual=False):
+    def forward(self, x_local, prompt, out_local, exchange, add_residual=False, stage_prefix="block0"):
         """x_local [F, vc_r, D] fp32 -> out_local [F, vc_r, D] fp32 (block
         output of the local rows, + x_local if add_residual)."""
-        return run_stages(self, x_local, prompt, out_local, exchange, add_residual)
+        return run_stages(self, x_local, prompt, out_local, exchange, add_residual, stage_prefix)
 
 
 def _half(buf, b):
@@ -207,27 +264,42 @@ def _half(buf, b):
     return buf[b * n:(b + 1) * n]
 
 
-def run_stages(stages, x_local, prompt, out_local, exchange, add_residual=False):
+def run_stages(stages, x_local, prompt, out_local, exchange, add_residual=False, stage_prefix="block0"):
     """The rank-local schedule with the exchange split by branch (the buffers
     are branch-major) so it overlaps compute:
 
-      stage1 -> a2a#1 spatial, a2a#1 full-seq (async, NCCL stream)
+      stage1 part 0 (LN + QKV GEMM into send1)
+        -> a2a#1 spatial, a2a#1 full-seq (async, NCCL stream)
+      stage1 part 1 (the rank-local temporal branch, under a2a#1)
       wait spatial   -> stage2 spatial  -> a2a#2 spatial (async)
       wait full-seq  -> stage2 full-seq -> a2a#2 full-seq (async)
       wait both      -> stage3
 
-    so the full-sequence q/k/v travel while the spatial attention runs and
-    the spatial outputs travel while the full-sequence attention runs.
-    `stages` provides stage1/2/3, the four exchange buffers and per-peer counts
-    (SPBlock on the GPU; a numpy stand-in in the CPU gloo test)."""
+    so the q/k/v travel while the temporal branch runs, the full-sequence
+    q/k/v while the spatial attention runs, and the spatial outputs while the
+    full-sequence attention runs. `stages` provides stage1/2/3, the four
+    exchange buffers and per-peer counts (SPBlock on the GPU; a numpy
+    stand-in in the CPU gloo test). With a LoggedExchange every collective is
+    recorded under f"{stage_prefix}.spatial" / ".fullseq" (executor.py:571-626)."""
     bc = branch_counts(stages.counts)
-    stages.stage1(x_local, prompt)
-    h1 = [exchange.all_to_all(_half(stages.recv1, b), _half(stages.send1, b), bc["recv1"], bc["send1"],
-                              async_op=True) for b in (0, 1)]
+    ref = getattr(stages, "payload_counts", None)
+    ref = branch_counts(ref) if ref else None
+    stages.stage1(x_local, prompt, part=0)
+    h1 = []
+    for b, name in ((0, "spatial"), (1, "fullseq")):
+        if isinstance(exchange, LoggedExchange):
+            exchange.stage = f"{stage_prefix}.{name}"
+            exchange.payload = sum(ref["send1"]) if ref else None
+        h1.append(exchange.all_to_all(_half(stages.recv1, b), _half(stages.send1, b), bc["recv1"], bc["send1"],
+                                      async_op=True))
+    stages.stage1(x_local, prompt, part=1)
     h2 = []
-    for b in (0, 1):
+    for b, name in ((0, "spatial"), (1, "fullseq")):
         h1[b].wait()
         stages.stage2(b)
+        if isinstance(exchange, LoggedExchange):
+            exchange.stage = f"{stage_prefix}.{name}"
+            exchange.payload = sum(ref["send2"]) if ref else None
         h2.append(exchange.all_to_all(_half(stages.recv2, b), _half(stages.send2, b), bc["recv2"], bc["send2"],
                                       async_op=True))
     for h in h2:
@@ -446,14 +518,17 @@ def sp_model_forward(torch, model, latents, t, prompt, spb_cache, exchange, rank
     spb = spb_cache[key]
     lo, hi = spb.local_rows
     x = embed_rows(torch, model, lat, t, lo, hi - lo)
-    for db in dbs:
+    for bi, db in enumerate(dbs):
         spb.db = db
-        spb.forward(x, pr, x, exchange, add_residual=True)
+        spb.forward(x, pr, x, exchange, add_residual=True, stage_prefix=f"block{bi}")
     # all-gather the rows (uneven shards: pad to the largest, gather, trim)
     vmax = max(spb.vb[r + 1] - spb.vb[r] for r in range(nranks))
     pad = torch.zeros((F, vmax, model.dim), dtype=torch.float32, device="cuda")
     pad[:, :hi - lo] = x
     allx = torch.empty((nranks, F, vmax, model.dim), dtype=torch.float32, device="cuda")
+    if isinstance(exchange, LoggedExchange):  # executor.py:683-693 "gather" (fp32 rows here)
+        exchange.log.record("gather", "allgather", nranks, exchange.placement, pad.numel() * 4,
+                            F * (hi - lo) * model.dim * 4)
     dist.all_gather_into_tensor(allx, pad, group=group)
     full = torch.cat([allx[r, :, :spb.vb[r + 1] - spb.vb[r]] for r in range(nranks)], dim=1).contiguous()
     return unembed(torch, model, full, h, w, c)
@@ -556,8 +631,14 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
     torch.cuda.synchronize()
     e2e = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    # one untimed forward with the collectives logged (executor.py:111-141 CommLog rows)
+    comm = CommLog()
+    spb.forward(x_local, prompt, out, LoggedExchange(ex, comm, world, bpe=2))
+    torch.cuda.synchronize()
     # the exchanges alone (untimed pass): NVLink GB/s per rank, max time over ranks
-    a2a = {"mode": mode}
+    a2a = {"mode": mode, "comm_log": [[*e.key(), e.payload_bytes] for e in comm.events],
+           "comm_log_fields": ["stage", "collective", "group_size", "placement", "bytes_per_device (as sent)",
+                               "payload_bytes (reference payload: no head-dim padding)"]}
     if mode == "head_parallel":
         t = time_exchanges(torch, spb, ex)
         tt = torch.tensor([t[k] for k in sorted(t)], device="cuda")

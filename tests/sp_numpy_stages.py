@@ -29,11 +29,14 @@ class NumpyStages:
         self.vb = sp.contiguous_bounds(Lv, P)
         self.M = [F * (self.vb[r + 1] - self.vb[r]) for r in range(P)]
         self.counts = sp.exchange_counts(F, Lv, H, D, P, rank)
+        self.payload_counts = sp.exchange_counts(F, Lv, H, D, P, rank, padded=False)
         mk = lambda k: torch.zeros(sum(self.counts[k]), dtype=torch.float64)  # noqa: E731
         self.send1, self.recv1, self.send2, self.recv2 = mk("send1"), mk("recv1"), mk("send2"), mk("recv2")
 
     # stage 1: local rows -> q/k/v by head group + local temporal branch
-    def stage1(self, x_local, prompt):
+    def stage1(self, x_local, prompt, part=2):
+        if part == 1:  # the temporal branch (part 1) is folded into stage3 here
+            return
         F, D, Hg, DP, dh = self.F, self.D, self.Hg, self.DP, self.dh
         xl = x_local.numpy()
         vc = xl.shape[1]

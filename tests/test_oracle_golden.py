@@ -160,3 +160,14 @@ def test_frame_slices_equal_full_forward():
     fs = FrameSlices(blk, x, prompt, H, q_chunk=7)
     for f in (2, 0, 3, 1, 2):
         np.testing.assert_allclose(fs.step(f), full[f], atol=1e-12)
+
+
+def test_comm_plan_restatement_equals_reference_executor_log():
+    # executor.py:721-773 restated; the reference's own run_sp_iteration log
+    # (golden) for the toy model: 3 frames, 4 visual + 3 text tokens, D 12, H 6
+    for P in (2, 3):
+        rows = O.comm_plan(3, 3, 4, 12, 6, 1, P)
+        assert [r[4] for r in rows] == [float(b) for b in G[f"sp_p{P}_comm"]]
+        assert [r[:2] for r in rows] == [("reshard", "alltoall"), ("block0.spatial", "alltoall"),
+                                         ("block0.spatial", "alltoall"), ("block0.fullseq", "alltoall"),
+                                         ("block0.fullseq", "alltoall"), ("gather", "allgather")]

@@ -93,3 +93,62 @@ def test_sp_gather_gloo_equals_single_device(world, add_residual):
         mp.spawn(_worker, args=(world, _free_port(), d, add_residual, "gather", sh), nprocs=world, join=True)
         got = np.concatenate([np.load(os.path.join(d, f"out{r}.npy")) for r in range(world)], axis=1)
     np.testing.assert_allclose(got, ref, atol=1e-10, rtol=0)
+
+
+def _log_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import json
+
+    import torch.distributed as dist
+
+    from paper_2501_08453_b200 import sp
+    from sp_numpy_stages import NumpyStages
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sh = SHAPE
+        blk, x, prompt = _case(sh)
+        st = NumpyStages(blk, sh["F"], sh["Lv"], sh["Lt"], sh["D"], sh["H"], world, rank)
+        lo, hi = st.vb[rank], st.vb[rank + 1]
+        xl = torch.from_numpy(np.ascontiguousarray(x[:, lo:hi]))
+        log = sp.CommLog()
+        ex = sp.LoggedExchange(sp.TorchExchange(), log, world, bpe=8)  # the stand-in exchanges fp64
+        sp.run_stages(st, xl, torch.from_numpy(prompt), torch.empty_like(xl), ex, stage_prefix="block0")
+        with open(os.path.join(outdir, f"log{rank}.json"), "w") as f:
+            json.dump([[*e.key(), e.payload_bytes] for e in log.events], f)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_logged_collectives_match_reference_comm_plan(world):
+    # the CommLog of the collectives the product's driver really issues
+    # (executor.py:111-141 fields) against the reference's schedule
+    # (executor.py:721-773, oracle.comm_plan, pinned to the reference's log):
+    # same stages, collectives, group and placement in the same order; the
+    # payload bytes (largest rank, as the reference logs) equal, except the
+    # full-sequence a2a #1, which does not ship the text rows (every rank
+    # projects them from its own prompt copy); no "reshard" (each rank embeds
+    # its own rows) -- and the "gather" is sp_model_forward's, not run_stages'
+    import json
+
+    from oracle import spsim_oracle as O
+    sh = SHAPE
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_log_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        logs = [json.load(open(os.path.join(d, f"log{r}.json"))) for r in range(world)]
+    ref = O.comm_plan(sh["F"], sh["Lt"], sh["Lv"], sh["D"], sh["H"], 1, world)
+    ref_block = [r for r in ref if r[0].startswith("block0")]
+    # issue order differs by design (both branches' a2a #1 go out before
+    # either attention, to overlap them): compare each stage's own sequence
+    order = {"block0.spatial": 0, "block0.fullseq": 1}
+    logs = [sorted(log, key=lambda e: order[e[0]]) for log in logs]  # stable: per-stage order kept
+    assert all([tuple(e[:4]) for e in log] == [tuple(r[:4]) for r in ref_block] for log in logs)
+    payload = [max(log[i][5] for log in logs) for i in range(len(ref_block))]
+    tb = O.contiguous_bounds(sh["Lt"], world)
+    text_rows = sh["F"] * max(tb[r + 1] - tb[r] for r in range(world))
+    expect = [r[4] for r in ref_block]
+    expect[2] -= 3 * text_rows * sh["D"] * 8  # full-sequence a2a #1: no text rows on the wire
+    assert payload == expect
