@@ -9,8 +9,10 @@ module gives:
 
 * `B200Spec` — the same fields and SI units with this pool's B200 values: the
   measured sustained bf16 rate and HBM size, the measured pinned host copy
-  rate (bench e2e), NVLink 5 per-direction bandwidth (nominal; NCCL is not
-  measurable on the one-GPU pool) and an assumed NCCL latency.
+  rate (bench e2e), NVLink 5 per-direction bandwidth (nominal: NCCL across
+  GPUs is not measurable on the one-GPU pool; bench.py --sp reports the
+  world-1 exchange times, which are local copies) and an assumed NCCL
+  latency.
   `as_cluster_kwargs()` builds the reference's own `ClusterSpec(**kwargs)`.
 * `alltoall_time` — the reference's all-to-all formula (cluster.py:112-118).
 * `price_sp_block` — one block forward on P ranks of this implementation's
@@ -20,8 +22,9 @@ module gives:
   attentions), plus the two per-branch all-to-alls priced with the exact byte
   counts this implementation sends (`sp.exchange_counts`: q, k, v with the
   head dim padded to 80), either fully exposed or overlapped the way
-  `sp.run_stages` overlaps them (a branch's exchange under the other
-  branch's attention).
+  `sp.run_stages` schedules them (both a2a #1 under the temporal branch and
+  the spatial attention, a2a #2 of the spatial branch under the
+  full-sequence attention).
 
 These are PRICED numbers (a model), not measurements; profiles/ labels them
 so. Pure host code: no GPU needed.
@@ -93,13 +96,21 @@ def price_sp_block(stage_ms: dict, frames: int, visual_len: int, text_len: int, 
     if not overlap or p == 1:
         exposed = comm
     else:
-        # sp.run_stages: a2a#1(spatial) is exposed (nothing to hide it but the
-        # temporal branch), a2a#1(full seq) runs under the spatial attention,
-        # a2a#2(spatial) under the full-sequence attention, a2a#2(full seq) is
-        # exposed before the O projection
-        hide_tm = compute.get("attn_temporal", 0.0)
-        exposed = max(0.0, t1 - hide_tm) + max(0.0, t1 - compute.get("attn_spatial", 0.0)) \
-            + max(0.0, t2 - compute.get("attn_fullseq", 0.0)) + t2
+        # sp.run_stages (NCCL runs its collectives one after another on its
+        # own stream; compute on the main stream):
+        #   both a2a #1 start after the QKV GEMM; the temporal branch runs under them
+        #   spatial attention once a2a#1(spatial) landed; a2a#2(spatial) after it
+        #   full-seq attention once a2a#1(full seq) landed; a2a#2(full seq) after it
+        #   the O projection once both a2a #2 landed
+        tm = compute.get("attn_temporal", 0.0)
+        sp_att, fs_att = compute.get("attn_spatial", 0.0), compute.get("attn_fullseq", 0.0)
+        net = 2 * t1                      # NCCL stream busy until both a2a #1 are done
+        a1_sp, a1_fs = t1, 2 * t1
+        sp_end = max(tm, a1_sp) + sp_att
+        a2_sp = max(sp_end, net) + t2
+        fs_end = max(sp_end, a1_fs) + fs_att
+        a2_fs = max(fs_end, a2_sp) + t2
+        exposed = a2_fs - (tm + sp_att + fs_att)  # the critical path beyond the compute it overlaps
     layout = sp_overhead_ms * row_share if p > 1 else 0.0
     total = sum(compute.values()) + layout + exposed
     return {"p": p, "ms": total, "compute_ms": sum(compute.values()) + layout, "comm_ms": comm,
