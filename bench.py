@@ -501,7 +501,7 @@ def run_gpu_sp(args, torch, world, rank, local):
     from paper_2501_08453_b200 import sp
     return sp.bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops,
                        load_peaks, tensor_peak, ClockSampler, cpu_slices, time_slices, slice_sample_text,
-                       cpu_cores)
+                       cpu_cores, stage_profile)
 
 
 def main():

@@ -234,6 +234,17 @@ VC_API size_t vc_sp_workspace_bytes(const vc_sp_plan* plan);
  * peer (bf16 elements as laid out: head dim padded to DP, dh-66 outputs in
  * DP-wide head slots); 4..7 the same without that padding (the reference's
  * payload, executor.py:344-347, :395-412). -1 on error. */
+/* Frame-wise -> spatial reshard (alltoall_reshard, executor.py:252-287,
+ * spatial axis): rank d holds the embedded frames f = d, d+P, ... (the
+ * round-robin deal, executor.py:194-196) as [n_d][Lv][D] fp32; pack writes
+ * the send buffer (peer r gets rows [vb[r], vb[r+1]) of each), all_to_all,
+ * unpack writes the resident [F][vc_rank][D]. which 0: send elements to
+ * peer, 1: receive elements from peer (fp32). Resident equal to
+ * allgather_then_shard (executor.py:290-308) exactly. */
+VC_API int64_t vc_sp_reshard_elems(const vc_sp_plan* plan, int32_t which, int32_t peer);
+VC_API int vc_sp_reshard_pack(const vc_sp_plan* plan, const float* local_frames, float* send, void* stream);
+VC_API int vc_sp_reshard_unpack(const vc_sp_plan* plan, const float* recv, float* resident, void* stream);
+
 /* The row maps the exchanges use (exact-equality tests against the
  * reference's stable argsort, executor.py:349-370, :606-617). which 0: for
  * the rows of every rank concatenated in rank order (each rank's local rows

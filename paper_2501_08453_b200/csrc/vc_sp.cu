@@ -352,6 +352,64 @@ __global__ void __launch_bounds__(256) spg_unpack_vt_kernel(SpgUnpack a) {
   }
 }
 
+// Frame-wise -> spatial reshard (executor.py:252-287, spatial axis): rank d
+// embeds the frames f = d, d + P, ... (round_robin_frames, executor.py:194-196);
+// every peer r receives rows [vb[r], vb[r+1]) of each of them.  One warp per
+// row, 16-byte copies (D % 4 == 0).
+struct ReshardArgs {
+  int32_t P, rank, F, Lv, D;
+  int32_t vb[17];
+  int64_t off[17];  // per-peer block offsets (elements) in the send / recv buffer
+};
+__device__ __forceinline__ int frames_of(int F, int P, int d) { return d < F ? (F - d + P - 1) / P : 0; }
+
+__global__ void __launch_bounds__(256) reshard_pack_kernel(const float* __restrict__ local, float* __restrict__ send,
+                                                           ReshardArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int nf = frames_of(a.F, a.P, a.rank);
+  const int64_t rows = (int64_t)nf * a.Lv;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int i = (int)(w / a.Lv), l = (int)(w - (int64_t)i * a.Lv);  // my i-th frame, position l
+    const int r = sp_owner(a.vb, a.P, l);
+    const int vc = a.vb[r + 1] - a.vb[r];
+    const float4* src = reinterpret_cast<const float4*>(local + w * a.D);
+    float4* dst = reinterpret_cast<float4*>(send + a.off[r] + ((int64_t)i * vc + (l - a.vb[r])) * a.D);
+    for (int c = lane; c < a.D / 4; c += 32) dst[c] = src[c];
+  }
+}
+
+__global__ void __launch_bounds__(256) reshard_unpack_kernel(const float* __restrict__ recv, float* __restrict__ resident,
+                                                             ReshardArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int vc = a.vb[a.rank + 1] - a.vb[a.rank];
+  const int64_t rows = (int64_t)a.F * vc;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int f = (int)(w / vc), lp = (int)(w - (int64_t)f * vc);  // resident row (frame f, local position lp)
+    const int s = f % a.P, i = f / a.P;                            // source rank, its i-th frame
+    const float4* src = reinterpret_cast<const float4*>(recv + a.off[s] + ((int64_t)i * vc + lp) * a.D);
+    float4* dst = reinterpret_cast<float4*>(resident + w * a.D);
+    for (int c = lane; c < a.D / 4; c += 32) dst[c] = src[c];
+  }
+}
+
+int reshard_args(const Sp& x, int which, ReshardArgs* a) {
+  if (x.D % 4) { set_error("reshard needs dim %% 4 == 0"); return VC_EINVAL; }
+  a->P = (int)x.P; a->rank = (int)x.rank; a->F = (int)x.F; a->Lv = (int)x.Lv; a->D = (int)x.D;
+  for (int r = 0; r <= x.P; ++r) a->vb[r] = x.vb[r];
+  int64_t o = 0;
+  for (int r = 0; r < x.P; ++r) {
+    a->off[r] = o;
+    const int nf = which == 0 ? (x.rank < x.F ? (int)((x.F - x.rank + x.P - 1) / x.P) : 0)
+                              : (r < x.F ? (int)((x.F - r + x.P - 1) / x.P) : 0);
+    const int vc = which == 0 ? x.vb[r + 1] - x.vb[r] : x.vb[x.rank + 1] - x.vb[x.rank];
+    o += (int64_t)nf * vc * x.D;
+  }
+  a->off[x.P] = o;
+  return VC_OK;
+}
+
 }  // namespace
 
 }  // namespace vc
@@ -398,6 +456,40 @@ int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which, int32_t peer
   return -1;
 }
 
+int64_t vc_sp_reshard_elems(const vc_sp_plan* plan, int32_t which, int32_t peer) {
+  Sp x;
+  if (sp_make(plan, &x, true, true) != VC_OK || peer < 0 || peer >= x.P || which < 0 || which > 1) return -1;
+  ReshardArgs a;
+  if (reshard_args(x, which, &a) != VC_OK) return -1;
+  return a.off[peer + 1] - a.off[peer];
+}
+
+int vc_sp_reshard_pack(const vc_sp_plan* plan, const float* local_frames, float* send, void* stream) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x, true, true));  // any P <= Lv (no head-group condition), fp32 rows
+  ReshardArgs a;
+  VC_TRY(reshard_args(x, 0, &a));
+  const int64_t rows = (int64_t)(x.rank < x.F ? (x.F - x.rank + x.P - 1) / x.P : 0) * x.Lv;
+  if (rows == 0) return VC_OK;
+  const int blocks = (int)std::min<int64_t>(cdiv(rows, 8), 148 * 16);
+  reshard_pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(local_frames, send, a);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
+int vc_sp_reshard_unpack(const vc_sp_plan* plan, const float* recv, float* resident, void* stream) {
+  Sp x;
+  VC_TRY(sp_make(plan, &x, true, true));
+  ReshardArgs a;
+  VC_TRY(reshard_args(x, 1, &a));
+  const int64_t rows = x.F * (int64_t)(x.vb[x.rank + 1] - x.vb[x.rank]);
+  if (rows == 0) return VC_OK;
+  const int blocks = (int)std::min<int64_t>(cdiv(rows, 8), 148 * 16);
+  reshard_unpack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(recv, resident, a);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
+
 int vc_sp_row_map(const vc_sp_plan* plan, int32_t which, int64_t* out) {
   Sp x;
   VC_TRY(sp_make(plan, &x, false, true));
@@ -436,6 +528,7 @@ int vc_sp_stage1_part(const vc_sp_plan* plan, const void* packed, const float* x
   const SpWs w = sp_ws(x);
   if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
+  profile_begin(st);
   char* W = (char*)ws;
   typedef __nv_bfloat16 bf;
   const PackedPtrs pp = packed_ptrs(x, packed);
@@ -463,6 +556,7 @@ int vc_sp_stage1_part(const vc_sp_plan* plan, const void* packed, const float* x
                                (int)x.S));
     profile_mark(st, "sp_attn_temporal");
   }
+  profile_end();
   return VC_OK;
 }
 
@@ -474,6 +568,7 @@ int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed, const void* 
   if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
   if (branch < 0 || branch > 1) { set_error("branch must be 0 (spatial) or 1 (full sequence)"); return VC_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
+  profile_begin(st);
   char* W = (char*)ws;
   typedef __nv_bfloat16 bf;
   const PackedPtrs pp = packed_ptrs(x, packed);
@@ -526,6 +621,7 @@ int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed, const void* 
     VC_TRY(launch_attn_tc(a, fs.q, fs.k, fs.vt, 1, x.Nv, x.Lt + x.Nv, x.Lk_ld, (int)x.DP, st));
     profile_mark(st, "sp_attn_fullseq");
   }
+  profile_end();
   return VC_OK;
 }
 
@@ -542,6 +638,7 @@ int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, 
   const SpWs w = sp_ws(x);
   if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
+  profile_begin(st);
   typedef __nv_bfloat16 bf;
   const PackedPtrs pp = packed_ptrs(x, packed);
   const int64_t Mr = x.M[x.rank];
@@ -559,6 +656,7 @@ int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, 
   g.out_f32 = out_local; g.ldo = x.D; g.R = add_residual ? x_local : nullptr; g.ldr = x.D;
   VC_TRY(launch_gemm_tc(acat, 3 * x.BW, x.S ? pp.wo_s : pp.wo, 3 * x.BW, g, EPI_F32, st));
   profile_mark(st, "sp_oproj_gemm");
+  profile_end();
   return VC_OK;
 }
 
@@ -589,6 +687,7 @@ int vc_spg_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loc
   const SpgSlot gs = spg_slot(x);
   if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
+  profile_begin(st);
   char* W = (char*)ws;
   typedef __nv_bfloat16 bf;
   const PackedPtrs pp = packed_ptrs(x, packed);
@@ -626,6 +725,7 @@ int vc_spg_stage1(const vc_sp_plan* plan, const void* packed, const float* x_loc
     VC_TRY(launch_gemm_tc(xhat + Mr * x.D, x.D, pp.wqkv + n0 * x.D, x.D, g, EPI_QKV, st));
     profile_mark(st, "spg_text_kv_gemm");
   }
+  profile_end();
   return VC_OK;
 }
 
@@ -637,6 +737,7 @@ int vc_spg_stage2(const vc_sp_plan* plan, const void* packed, const void* gather
   const SpgSlot gs = spg_slot(x);
   if (ws_bytes < w.total) { set_error("SP workspace too small"); return VC_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
+  profile_begin(st);
   char* W = (char*)ws;
   typedef __nv_bfloat16 bf;
   const PackedPtrs pp = packed_ptrs(x, packed);
@@ -682,6 +783,7 @@ int vc_spg_stage2(const vc_sp_plan* plan, const void* packed, const void* gather
   g.out_f32 = out_local; g.ldo = x.D; g.R = add_residual ? x_local : nullptr; g.ldr = x.D;
   VC_TRY(launch_gemm_tc(acat, 3 * x.D, pp.wo, 3 * x.D, g, EPI_F32, st));
   profile_mark(st, "spg_oproj_gemm");
+  profile_end();
   return VC_OK;
 }
 

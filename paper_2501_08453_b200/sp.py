@@ -450,6 +450,72 @@ def emulate_sp_forward(torch, device_block, x, prompt, nranks, add_residual=Fals
 # Sequence-parallel model step: ToyDenoiser.forward over P ranks
 # ---------------------------------------------------------------------------
 
+class FrameReshard:
+    """Frame-wise -> spatial reshard of the embedded tokens (alltoall_reshard,
+    executor.py:252-287, spatial axis): this rank embedded the frames
+    round_robin_frames(F, P)[rank] = rank, rank + P, ... (executor.py:194-196)
+    and every peer r needs rows [vb[r], vb[r+1]) of each. CUDA pack / unpack
+    (vc_sp_reshard_*) around one all-to-all; the resident [F, vc_rank, D]
+    equals allgather_then_shard (executor.py:290-308) exactly."""
+
+    def __init__(self, torch, frames, visual_len, dim, heads, nranks, rank):
+        self.torch, self.F, self.Lv, self.D, self.P, self.rank = torch, frames, visual_len, dim, nranks, rank
+        self.plan = _lib.SpPlan(_lib.shape(frames, visual_len, 0, dim, heads, "bf16"), nranks, rank)
+        lib = _lib.load()
+        self.counts = {k: [int(lib.vc_sp_reshard_elems(C.byref(self.plan), i, r)) for r in range(nranks)]
+                       for i, k in enumerate(("send", "recv"))}
+        if min(self.counts["send"] + self.counts["recv"]) < 0:
+            raise ValueError(lib.vc_last_error().decode())
+        self.vb = contiguous_bounds(visual_len, nranks)
+        self.send = torch.empty(max(sum(self.counts["send"]), 1), dtype=torch.float32, device="cuda")
+        self.recv = torch.empty(max(sum(self.counts["recv"]), 1), dtype=torch.float32, device="cuda")
+
+    @property
+    def frames(self):
+        return list(range(self.rank, self.F, self.P))
+
+    def pack(self, local_frames):
+        lib = _lib.load()
+        _lib.check(lib.vc_sp_reshard_pack(C.byref(self.plan), _lib.ptr(local_frames), _lib.ptr(self.send),
+                                          _lib.stream_ptr(self.torch)), "reshard pack")
+
+    def unpack(self, resident):
+        lib = _lib.load()
+        _lib.check(lib.vc_sp_reshard_unpack(C.byref(self.plan), _lib.ptr(self.recv), _lib.ptr(resident),
+                                            _lib.stream_ptr(self.torch)), "reshard unpack")
+
+    def __call__(self, local_frames, exchange):
+        """local_frames [len(frames), Lv, D] fp32 -> resident [F, vc_rank, D] fp32."""
+        resident = self.torch.empty((self.F, self.vb[self.rank + 1] - self.vb[self.rank], self.D),
+                                    dtype=self.torch.float32, device="cuda")
+        self.pack(local_frames)
+        if isinstance(exchange, LoggedExchange):
+            exchange.stage = "reshard"
+            exchange.payload = None
+            exchange.bpe, bpe = 4, exchange.bpe
+        exchange.all_to_all(self.recv[:sum(self.counts["recv"])], self.send[:sum(self.counts["send"])],
+                            self.counts["recv"], self.counts["send"])
+        if isinstance(exchange, LoggedExchange):
+            exchange.bpe = bpe
+        self.unpack(resident)
+        return resident
+
+
+def embed_frames_local(torch, model, lat_dev, t, frames):
+    """ToyDenoiser.embed_frame (model.py:303-314) for the given frames -> [n, Lv, D] fp32."""
+    from .numerics import to_device_f32
+    F, h, w, c = lat_dev.shape
+    p = model.spec.patch
+    Lv = -(-h // p) * -(-w // p)
+    out = torch.empty((len(frames), Lv, model.dim), dtype=torch.float32, device="cuda")
+    w_in = to_device_f32(torch, model.w_in)
+    lib = _lib.load()
+    for i, f in enumerate(frames):
+        _lib.check(lib.vc_embed_frames(_lib.ptr(lat_dev[f:f + 1]), _lib.ptr(w_in), _lib.ptr(out[i:i + 1]), 1, f,
+                                       h, w, c, p, model.dim, float(t), _lib.stream_ptr(torch)), "embed frame")
+    return out
+
+
 def embed_rows(torch, model, lat_dev, t, tok0, ntok):
     """Rows [tok0, tok0+ntok) of every frame of ToyDenoiser.embed_frame
     (model.py:303-314) -> [F, ntok, D] fp32. Position-wise, so a rank embeds
@@ -477,7 +543,27 @@ def unembed(torch, model, x_full, h, w, c):
     return eps
 
 
-def emulate_sp_model_forward(torch, model, latents, t, prompt, nranks):
+def emulate_reshard(torch, reshards, locals_):
+    """FrameReshard over P virtual ranks on one GPU: pack everywhere, the
+    all-to-all as block copies with the product's per-peer counts, unpack."""
+    P = len(reshards)
+    for r, rs in enumerate(reshards):
+        rs.pack(locals_[r])
+    for dst in range(P):
+        pieces = []
+        for src in range(P):
+            off = sum(reshards[src].counts["send"][:dst])
+            pieces.append(reshards[src].send[off:off + reshards[src].counts["send"][dst]])
+        torch.cat(pieces, out=reshards[dst].recv[:sum(reshards[dst].counts["recv"])])
+    out = []
+    for r, rs in enumerate(reshards):
+        res = torch.empty((rs.F, rs.vb[r + 1] - rs.vb[r], rs.D), dtype=torch.float32, device="cuda")
+        rs.unpack(res)
+        out.append(res)
+    return out
+
+
+def emulate_sp_model_forward(torch, model, latents, t, prompt, nranks, embed="rows"):
     """ToyDenoiser.forward (bf16) over P virtual ranks: each rank embeds its
     rows, the blocks run sequence-parallel with the residual fused, the final
     all-gather (executor.py:683-693) becomes a concatenation, and the
@@ -491,13 +577,18 @@ def emulate_sp_model_forward(torch, model, latents, t, prompt, nranks):
     Lv = -(-h // p) * -(-w // p)
     dbs = [device_block(torch, b, model.heads, "bf16") for b in model.blocks]
     em = EmulatedRanks(torch, dbs[0], F, Lv, pr.shape[0], nranks)
-    xs = [embed_rows(torch, model, lat, t, em.vb[r], em.vb[r + 1] - em.vb[r]) for r in range(nranks)]
+    if embed == "frames":  # frame-wise embed on each rank + the reshard (executor.py:535-559)
+        rss = [FrameReshard(torch, F, Lv, model.dim, model.heads, nranks, r) for r in range(nranks)]
+        xs = emulate_reshard(torch, rss, [embed_frames_local(torch, model, lat, t, rs.frames) for rs in rss])
+    else:
+        xs = [embed_rows(torch, model, lat, t, em.vb[r], em.vb[r + 1] - em.vb[r]) for r in range(nranks)]
     for db in dbs:
         em.block_forward(xs, pr, xs, add_residual=True, device_block=db)
     return unembed(torch, model, torch.cat(xs, dim=1).contiguous(), h, w, c)
 
 
-def sp_model_forward(torch, model, latents, t, prompt, spb_cache, exchange, rank, nranks, group=None):
+def sp_model_forward(torch, model, latents, t, prompt, spb_cache, exchange, rank, nranks, group=None,
+                     embed="rows"):
     """ToyDenoiser.forward on this rank of a P-rank job (torchrun + NCCL):
     embed own rows -> depth x SPBlock.forward (residual fused, in place) ->
     all-gather the rows (executor.py:683-693) -> unembed. Every rank returns
@@ -517,7 +608,11 @@ def sp_model_forward(torch, model, latents, t, prompt, spb_cache, exchange, rank
         spb_cache[key] = SPBlock(torch, dbs[0], F, Lv, pr.shape[0], nranks, rank)
     spb = spb_cache[key]
     lo, hi = spb.local_rows
-    x = embed_rows(torch, model, lat, t, lo, hi - lo)
+    if embed == "frames":  # the reference's stage 1-2: frame-wise embed, then the reshard (executor.py:535-559)
+        rs = FrameReshard(torch, F, Lv, model.dim, model.heads, nranks, rank)
+        x = rs(embed_frames_local(torch, model, lat, t, rs.frames), exchange)
+    else:  # position-wise embed of the own rows: the same residents without a collective
+        x = embed_rows(torch, model, lat, t, lo, hi - lo)
     for bi, db in enumerate(dbs):
         spb.db = db
         spb.forward(x, pr, x, exchange, add_residual=True, stage_prefix=f"block{bi}")
@@ -562,7 +657,7 @@ def time_exchanges(torch, spb, ex, reps=5):
 
 
 def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops, load_peaks, tensor_peak,
-             ClockSampler, cpu_slices, time_slices, slice_sample_text, cpu_cores):
+             ClockSampler, cpu_slices, time_slices, slice_sample_text, cpu_cores, stage_profile=None):
     import json
     import torch.distributed as dist
 
@@ -631,6 +726,11 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
     torch.cuda.synchronize()
     e2e = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    # per-stage device time of this rank's kernels (untimed pass; the waits for
+    # the exchanges happen between the stage calls and are not counted)
+    stages_ms = None
+    if stage_profile is not None:
+        stages_ms = stage_profile(torch, _lib.load(), lambda: spb.forward(x_local, prompt, out, ex), 3)
     # one untimed forward with the collectives logged (executor.py:111-141 CommLog rows)
     comm = CommLog()
     spb.forward(x_local, prompt, out, LoggedExchange(ex, comm, world, bpe=2))
@@ -691,6 +791,7 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
                          "unit": "TFLOP/s", "frac": flops / world / (ms_per_step / 1e3) / 1e12 / peak,
                          "traffic": None, "peak_kind": peak_kind},
             "a2a": a2a,
+            "stage_ms": stages_ms,
             "cpu_baseline": cpu,
             "e2e": {"value": Nv / (float(e2e.item()) / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(xh.numel() * 4) * world, "d2h_bytes_per_step": int(oh.numel() * 4) * world},

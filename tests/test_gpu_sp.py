@@ -119,3 +119,35 @@ def test_sp_model_forward_matches_single_gpu(torch):
         got = sp.emulate_sp_model_forward(torch, model, lat, t, prompt, P).double().cpu().numpy()
         assert rel_l2(got, single) <= 1e-3, P
         assert rel_l2(got, ref) <= 2e-2, P
+        # the reference's own stage 1-2 (frame-wise embed + reshard) gives the
+        # same residents as the own-row embed: bitwise the same step
+        got_f = sp.emulate_sp_model_forward(torch, model, lat, t, prompt, P, embed="frames").double().cpu().numpy()
+        assert np.array_equal(got_f, got), P
+
+
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+def test_frame_reshard_equals_allgather_then_shard(torch, P):
+    # the frame-wise -> spatial reshard (alltoall_reshard,
+    # executor.py:252-287) through the CUDA pack / unpack and the product's
+    # per-peer counts (the all-to-all emulated by block copies) must equal
+    # allgather_then_shard (executor.py:290-308), the reference's oracle for
+    # it, exactly -- pure data movement, so bitwise
+    from paper_2501_08453_b200 import sp
+    F, Lv, D, H = 7, 37, 48, 4
+    g = torch.Generator(device="cuda").manual_seed(P)
+    full = torch.randn((F, Lv, D), device="cuda", generator=g)
+    rs = [sp.FrameReshard(torch, F, Lv, D, H, P, r) for r in range(P)]
+    for r in range(P):
+        assert rs[r].frames == [f for f in range(F) if f % P == r]  # round_robin_frames
+        rs[r].pack(full[rs[r].frames].contiguous())
+    for dst in range(P):  # recv of dst = the dst block of every source's send, in source order
+        pieces = []
+        for src in range(P):
+            off = sum(rs[src].counts["send"][:dst])
+            pieces.append(rs[src].send[off:off + rs[src].counts["send"][dst]])
+        torch.cat(pieces, out=rs[dst].recv[:sum(rs[dst].counts["recv"])])
+    vb = sp.contiguous_bounds(Lv, P)
+    for r in range(P):
+        res = torch.empty((F, vb[r + 1] - vb[r], D), device="cuda")
+        rs[r].unpack(res)
+        assert torch.equal(res, full[:, vb[r]:vb[r + 1]])

@@ -154,3 +154,25 @@ def test_sp_reassembly_order_equals_reference_stable_argsort(P):
     back = _row_map(F, Lv, Lt, D, H, P, 1)
     assert np.array_equal(back[tok], np.arange(F * Lv))
     assert sorted(back.tolist()) == list(range(F * Lv))
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_reshard_counts_match_reference_volume(P):
+    # alltoall_reshard's wire volume (executor.py:252-287): every peer gets
+    # the rows it owns of each of the sender's frames; the C ABI's per-peer
+    # counts (fp32 elements) reproduce the reference's exact "sent" bytes
+    from oracle import spsim_oracle as O
+    lib = _lib.load()
+    F, Lv, D, H = 7, 37, 48, 4
+    vb = O.contiguous_bounds(Lv, P)
+    deal = O.round_robin_frames(F, P)
+    sent_ref = sum(len(deal[src]) * (vb[dst + 1] - vb[dst]) * D for src in range(P) for dst in range(P) if src != dst)
+    sent = 0
+    for r in range(P):
+        plan = _lib.SpPlan(_lib.shape(F, Lv, 0, D, H, "bf16"), P, r)
+        send = [lib.vc_sp_reshard_elems(C.byref(plan), 0, g) for g in range(P)]
+        recv = [lib.vc_sp_reshard_elems(C.byref(plan), 1, g) for g in range(P)]
+        assert send == [len(deal[r]) * (vb[g + 1] - vb[g]) * D for g in range(P)]
+        assert recv == [len(deal[g]) * (vb[r + 1] - vb[r]) * D for g in range(P)]
+        sent += sum(send) - send[r]
+    assert sent == sent_ref
