@@ -157,6 +157,16 @@ VC_API int vc_embed_frames(const float* latents_dev, const float* w_in_dev,
                     int32_t h, int32_t w, int32_t c, int32_t patch,
                     int32_t dim, double t, void* stream);
 
+/* toy_vae_encode (model.py:381-403) of F frames [F][H][W][3] fp32 ->
+ * latents [F][ceil(H/d)][ceil(W/d)][channels] fp32 (zero-padded d x d block
+ * average, fixed cosine channel mix), optionally with q_sample
+ * (diffusion.py:77-84) fused: latents = sqrt_alpha_bar * encode +
+ * sqrt_one_minus_alpha_bar * noise (noise [F][gh][gw][channels]; NULL for the
+ * plain encode: pass 1, 0). channels <= 16. */
+VC_API int vc_vae_encode_frames(const float* pixels_dev, const float* noise_dev, float* latents_dev, int32_t F,
+                                int32_t H, int32_t W, int32_t downsample, int32_t channels, double sqrt_alpha_bar,
+                                double sqrt_one_minus_alpha_bar, void* stream);
+
 /* Row subset of vc_embed_frames: tokens [tok0, tok0+ntok) of every frame ->
  * x [F][ntok][D]. A sequence-parallel rank embeds its own rows directly
  * (the embedding is position-wise), replacing the reference's frame-wise

@@ -310,6 +310,23 @@ def parallel_block_rows(block, visual, text, heads, f_idx, l_idx):
     return out
 
 
+def _channel_mix(channels):
+    """model.py:399-403 -- fixed [3, C] cosine projection."""
+    j = np.arange(3)[:, None]
+    i = np.arange(channels)[None, :]
+    return math.sqrt(2.0 / 3.0) * np.cos(math.pi * (2 * j + 1) * i / 6.0)
+
+
+def toy_vae_encode(frame, spec=PatchSpec()):
+    """model.py:381-396 -- zero-pad to a multiple of d, d x d block mean, channel mix."""
+    d = spec.vae_downsample
+    h, w, _ = frame.shape
+    gh, gw = math.ceil(h / d), math.ceil(w / d)
+    padded = np.zeros((gh * d, gw * d, 3))
+    padded[:h, :w] = frame
+    return padded.reshape(gh, d, gw, d, 3).mean(axis=(1, 3)) @ _channel_mix(spec.latent_channels)
+
+
 @dataclass
 class ToyDenoiser:
     """model.py:274-333."""
@@ -365,6 +382,12 @@ def make_linear_schedule(steps, beta_start=1e-4, beta_end=0.02):
     alphas = 1.0 - betas
     abar = np.cumprod(alphas)
     return {"betas": betas, "alphas": alphas, "alpha_bars": abar, "omab": 1.0 - abar}
+
+
+def q_sample(schedule, x0, t, noise):
+    """diffusion.py:77-84 -- x_t in closed form from clean data."""
+    i = t - 1
+    return np.sqrt(schedule["alpha_bars"][i]) * x0 + np.sqrt(schedule["omab"][i]) * noise
 
 
 def reverse_step(schedule, x_t, t, predicted_noise, injected_noise=None):

@@ -18,6 +18,7 @@ from .model import (  # noqa: F401
     seq_len,
     spatial_branch,
     temporal_branch,
+    toy_vae_encode,
 )
 from .numerics import SeededRng, attention  # noqa: F401
 

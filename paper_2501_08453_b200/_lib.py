@@ -66,6 +66,7 @@ SIGNATURES = {
     "vc_sp_workspace_bytes": (_sz, [C.POINTER(SpPlan)]),
     "vc_sp_exchange_elems": (_i64, [C.POINTER(SpPlan), _i32, _i32]),
     "vc_sp_row_map": (_i32, [C.POINTER(SpPlan), _i32, C.c_void_p]),
+    "vc_vae_encode_frames": (_i32, [_p, _p, _p, _i32, _i32, _i32, _i32, _i32, _d, _d, _p]),
     "vc_sp_reshard_elems": (_i64, [C.POINTER(SpPlan), _i32, _i32]),
     "vc_sp_reshard_pack": (_i32, [C.POINTER(SpPlan), _p, _p, _p]),
     "vc_sp_reshard_unpack": (_i32, [C.POINTER(SpPlan), _p, _p, _p]),

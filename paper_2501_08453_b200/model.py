@@ -333,6 +333,42 @@ def layer_norm(x, eps: float = 1e-5):
 
 
 # ---------------------------------------------------------------------------
+# The frame encoder (model.py:381-403) and forward noising (diffusion.py:77-84)
+# ---------------------------------------------------------------------------
+
+def encode_frames_device(torch, pixels_dev, spec: PatchSpec = PatchSpec(), schedule=None, t=None, noise_dev=None):
+    """toy_vae_encode of every frame of a device clip [F, H, W, 3] fp32 ->
+    latents [F, ceil(H/d), ceil(W/d), C] fp32, with q_sample (diffusion.py:77-84)
+    fused when a schedule, t and noise are given (vc_vae_encode_frames)."""
+    F, H, W, c = pixels_dev.shape
+    if c != 3:
+        raise ValueError(f"expected [h, w, 3] pixels, got {tuple(pixels_dev.shape[1:])}")
+    gh, gw = spec.latent_hw(H, W)
+    out = torch.empty((F, gh, gw, spec.latent_channels), dtype=torch.float32, device="cuda")
+    sab, somab = 1.0, 0.0
+    if noise_dev is not None:
+        i = schedule._idx(int(t))
+        sab, somab = math.sqrt(schedule.alpha_bars[i]), math.sqrt(schedule.one_minus_alpha_bars[i])
+    lib = _lib.load()
+    _lib.check(lib.vc_vae_encode_frames(_lib.ptr(pixels_dev), _lib.ptr(noise_dev), _lib.ptr(out), F, H, W,
+                                        spec.vae_downsample, spec.latent_channels, sab, somab,
+                                        _lib.stream_ptr(torch)), "vae encode")
+    return out
+
+
+def toy_vae_encode(frame, spec: PatchSpec = PatchSpec()):
+    """model.py:381-403 -- [h, w, 3] pixels -> [ceil(h/8), ceil(w/8), C] latents
+    (same signature and ValueError as the reference; on the GPU)."""
+    if frame.ndim != 3 or frame.shape[2] != 3:
+        raise ValueError(f"expected [h, w, 3] pixels, got {frame.shape}")
+    torch = _lib.require_cuda()
+    as_numpy = not _is_torch(frame)
+    px = to_device_f32(torch, frame)[None]
+    out = encode_frames_device(torch, px, spec)[0]
+    return out.double().cpu().numpy() if as_numpy else out
+
+
+# ---------------------------------------------------------------------------
 # The toy denoiser (model.py:274-333)
 # ---------------------------------------------------------------------------
 

@@ -145,6 +145,16 @@ def main():
         fixtures[f"sp_p{p}_pred"] = res.predicted_noise
         fixtures[f"sp_p{p}_comm"] = np.array([e.bytes_per_device for e in res.log.events])
 
+    # --- toy VAE encode (model.py:381-403) and q_sample (diffusion.py:77-84):
+    # ragged frame sizes (zero padding), 4 and 8 latent channels
+    from spsim.diffusion import q_sample
+    for h, w, c in ((32, 32, 4), (37, 29, 4), (20, 50, 8)):
+        frame = rn.SeededRng(900 + h).uniform((h, w, 3))
+        lat = rm.toy_vae_encode(frame, rm.PatchSpec(8, 2, c))
+        fixtures[f"vae_{h}x{w}_c{c}"] = lat
+        noise = rn.SeededRng(950 + h).normal(lat.shape)
+        fixtures[f"qs37_{h}x{w}_c{c}"] = q_sample(sched, lat, 37, noise)
+
     np.savez_compressed(os.path.join(OUT, "golden.npz"), **fixtures)
     print("wrote", os.path.join(OUT, "golden.npz"))
 

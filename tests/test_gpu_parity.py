@@ -293,3 +293,25 @@ def test_block_random_shapes_sweep(vc):
         if D % 8 == 0:
             got16 = vc.parallel_block_forward(blk, x, text, H, dtype="bf16")
             assert rel_l2(got16, ref) <= BF16_TOL, (case, F, Lv, Lt, D, H, rel_l2(got16, ref))
+
+
+def test_vae_encode_and_fused_q_sample_vs_golden(vc):
+    # the frame encoder + forward noising every rank runs on its round-robin
+    # frames (executor.py:535-546): vc_vae_encode_frames vs the reference
+    import torch
+
+    from paper_2501_08453_b200.diffusion import make_linear_schedule
+    from paper_2501_08453_b200.model import encode_frames_device
+    sched = make_linear_schedule(100)
+    for h, w, c in ((32, 32, 4), (37, 29, 4), (20, 50, 8)):
+        frame = vc.SeededRng(900 + h).uniform((h, w, 3))
+        spec = vc.PatchSpec(8, 2, c)
+        lat = vc.toy_vae_encode(frame, spec)
+        assert normwise(lat, G[f"vae_{h}x{w}_c{c}"]) <= 1e-6
+        noise = vc.SeededRng(950 + h).normal(lat.shape)
+        px = torch.from_numpy(frame[None].astype(np.float32)).cuda()
+        nz = torch.from_numpy(noise[None].astype(np.float32)).cuda()
+        got = encode_frames_device(torch, px, spec, sched, 37, nz)[0].double().cpu().numpy()
+        assert normwise(got, G[f"qs37_{h}x{w}_c{c}"]) <= 1e-6
+    with pytest.raises(ValueError, match="pixels"):
+        vc.toy_vae_encode(np.zeros((8, 8, 4)))

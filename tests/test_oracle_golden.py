@@ -171,3 +171,14 @@ def test_comm_plan_restatement_equals_reference_executor_log():
         assert [r[:2] for r in rows] == [("reshard", "alltoall"), ("block0.spatial", "alltoall"),
                                          ("block0.spatial", "alltoall"), ("block0.fullseq", "alltoall"),
                                          ("block0.fullseq", "alltoall"), ("gather", "allgather")]
+
+
+def test_vae_encode_and_q_sample_vs_reference():
+    # model.py:381-403 and diffusion.py:77-84, ragged frames (zero padding)
+    sched = O.make_linear_schedule(100)
+    for h, w, c in ((32, 32, 4), (37, 29, 4), (20, 50, 8)):
+        frame = O.SeededRng(900 + h).uniform((h, w, 3))
+        lat = O.toy_vae_encode(frame, O.PatchSpec(8, 2, c))
+        np.testing.assert_allclose(lat, G[f"vae_{h}x{w}_c{c}"], rtol=0, atol=1e-12)
+        noise = O.SeededRng(950 + h).normal(lat.shape)
+        np.testing.assert_allclose(O.q_sample(sched, lat, 37, noise), G[f"qs37_{h}x{w}_c{c}"], rtol=0, atol=1e-12)
