@@ -240,10 +240,6 @@ VC_API int vc_sp_check(const vc_sp_plan* plan);
 /* vbounds[0..P] = contiguous_bounds(Lv, P) (executor.py:187-191). */
 VC_API int vc_sp_bounds(const vc_sp_plan* plan, int32_t* vbounds);
 VC_API size_t vc_sp_workspace_bytes(const vc_sp_plan* plan);
-/* which: 0 send1 to peer, 1 recv1 from peer, 2 send2 to peer, 3 recv2 from
- * peer (bf16 elements as laid out: head dim padded to DP, dh-66 outputs in
- * DP-wide head slots); 4..7 the same without that padding (the reference's
- * payload, executor.py:344-347, :395-412). -1 on error. */
 /* Frame-wise -> spatial reshard (alltoall_reshard, executor.py:252-287,
  * spatial axis): rank d holds the embedded frames f = d, d+P, ... (the
  * round-robin deal, executor.py:194-196) as [n_d][Lv][D] fp32; pack writes
@@ -262,6 +258,12 @@ VC_API int vc_sp_reshard_unpack(const vc_sp_plan* plan, const float* recv, float
  * as (F*Lv entries); which 1: for each visual token, the index of the row it
  * is returned to by a2a #2 in that same concatenation. Host only. */
 VC_API int vc_sp_row_map(const vc_sp_plan* plan, int32_t which, int64_t* out);
+/* which: 0 send1 to peer, 1 recv1 from peer, 2 send2 to peer, 3 recv2 from
+ * peer (bf16 elements as laid out: head dim padded to DP, dh-66 outputs in
+ * DP-wide head slots; 0 for peer == rank: the own block never enters the
+ * buffers, stage 1 / 2 write it straight where stage 2 / 3 read it); 4..7
+ * the reference's payload (executor.py:344-347, :395-412): no padding, own
+ * block included. -1 on error. */
 VC_API int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which,
                                     int32_t peer);
 /* x_local [F][vc_r][D] fp32, prompt [Lt][D] fp32 -> send1 (bf16). */

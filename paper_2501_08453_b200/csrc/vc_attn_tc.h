@@ -15,6 +15,11 @@ struct SpOutMap {
   int64_t Dg;        // Hg * dh
   int32_t vb[17];
   int64_t base[17];
+  // own rank + 1 (0: none): rows this rank owns skip the exchange and go to
+  // self_out[row * self_ld] (the O GEMM's input; row = f * vc + l - vb[r])
+  int32_t self_r1;
+  int64_t self_ld;
+  __nv_bfloat16* self_out;
 };
 
 struct AttnTcParams {

@@ -127,6 +127,9 @@ __device__ __forceinline__ __nv_bfloat16* out_row(const AttnTcParams& p, int qi,
   const int f = p.spo.branch == 0 ? seq : qi / p.spo.Lv;
   const int lpos = p.spo.branch == 0 ? qi : qi - f * p.spo.Lv;
   const int r = sp_owner(p.spo.vb, p.spo.P, lpos);
+  if (r + 1 == p.spo.self_r1)
+    return p.spo.self_out + sp_token_to_row(p.spo.vb, r, f, lpos) * p.spo.self_ld +
+           (int64_t)h * (p.head_slot ? p.head_slot : p.dh);
   // base[r] already points at this branch's block for rank r
   return p.out + p.spo.base[r] + sp_token_to_row(p.spo.vb, r, f, lpos) * p.spo.Dg +
          (int64_t)h * (p.head_slot ? p.head_slot : p.dh);

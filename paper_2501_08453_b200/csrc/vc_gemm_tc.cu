@@ -46,7 +46,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 // ---- QKV scatter (EPI_QKV) ----
 // GEMM row m -> Q row / K row / (sequence, key) of the attention layouts.
-__device__ __forceinline__ int qkv_frame(const QkvScatter& s, int64_t m) { return (int)m / (int)s.Lv; }
+__device__ __forceinline__ int qkv_frame(const QkvScatter& s, int64_t m) { return (int)m / (s.Lf ? s.Lf : (int)s.Lv); }
 // sp_f: frame of row m (qkv_frame), hoisted out of the chunk loop by the caller
 __device__ __forceinline__ void qkv_rows(const QkvScatter& s, int b, int64_t m, int sp_f, int64_t& qrow,
                                          int64_t& krow, int64_t& seq, int64_t& key) {
@@ -151,7 +151,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
       int64_t row = m;
       if (s.tm_F) {  // position-major: row l*F + f
         const int fr = sp_f >= 0 ? sp_f : qkv_frame(s, m);
-        row = (m - (int64_t)fr * s.Lv) * s.tm_F + fr;
+        row = (m - (int64_t)fr * (s.Lf ? s.Lf : s.Lv)) * s.tm_F + fr;
       }
       __nv_bfloat16* o = s.tm + row * 3 * s.D + j;
       if (j + 16 <= 3 * s.D && n0 + 16 <= p.N) {
@@ -201,8 +201,35 @@ __device__ __forceinline__ void epilogue_chunk(const GemmTcParams& p, int64_t m,
     if (s.mode == 1) {  // sequence-parallel send layout, branch-major: [b'][g][which][m][Hg][DP]
       const int g = hg / s.Hg, hl = hg - g * s.Hg;
       const int P = s.H / s.Hg;
+      if (g + 1 == s.self_g) {  // own head group: straight into this rank's attention layouts
+        const BranchOut& bo = b == 0 ? s.sp : s.fs;
+        const int f = sp_f >= 0 ? sp_f : qkv_frame(s, m);
+        const int l = (int)m - f * s.Lf + s.self_v0;  // position in the frame
+        const int tok = f * (int)s.Lv + l;
+        __nv_bfloat16* o;
+        if (which < 2) {
+          const int64_t row = (which == 1 && b != 0) ? tok + s.Lt : tok;
+          o = (which == 0 ? bo.q : bo.k) + (row * s.Hg + hl) * q.DP + d0;
+        } else {  // V^T: 16 head dims of one key; lanes are consecutive keys (coalesced)
+          const int64_t seq = b == 0 ? f : 0, key = b == 0 ? l : tok + s.Lt;
+          __nv_bfloat16* vo = bo.vt + ((seq * s.Hg + hl) * q.DP + d0) * bo.ld_key + key;
+#pragma unroll
+          for (int i = 0; i < 16; ++i, vo += bo.ld_key) *vo = __float2bfloat16_rn(v[i]);
+          return;
+        }
+        uint4 a, c;
+        a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);
+        a.z = pack_bf16x2(v[4], v[5]); a.w = pack_bf16x2(v[6], v[7]);
+        c.x = pack_bf16x2(v[8], v[9]); c.y = pack_bf16x2(v[10], v[11]);
+        c.z = pack_bf16x2(v[12], v[13]); c.w = pack_bf16x2(v[14], v[15]);
+        reinterpret_cast<uint4*>(o)[0] = a;
+        reinterpret_cast<uint4*>(o)[1] = c;
+        return;
+      }
+      const int gs = (s.self_g && g >= s.self_g) ? g - 1 : g;  // slot among the sent groups
+      const int Ps = s.self_g ? P - 1 : P;
       const int64_t rowlen = (int64_t)s.Hg * q.DP;
-      __nv_bfloat16* o = s.send + ((int64_t)(b == 0 ? 0 : 1) * P + g) * 3 * s.send_rows * rowlen +
+      __nv_bfloat16* o = s.send + ((int64_t)(b == 0 ? 0 : 1) * Ps + gs) * 3 * s.send_rows * rowlen +
                          (which * s.send_rows + m) * rowlen + hl * q.DP + d0;
       uint4 a, c;
       a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]);

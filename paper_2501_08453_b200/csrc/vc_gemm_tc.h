@@ -36,6 +36,9 @@ struct QkvScatter {
   // rows l*F + f, so a position's F frames are consecutive rows (the
   // temporal attention's sequences, read as whole boxes)
   int32_t tm_F;
+  // GEMM rows per frame (0: Lv). The sequence-parallel stage 1 runs on a
+  // rank's local rows m = f * vc + l, so its frames are vc rows long.
+  int32_t Lf;
   // mode 1 (sequence-parallel send): spatial / full-seq Q, K, V of local row m
   // and head h go to send[b'][g][which][m][h % Hg][DP], g = h / Hg (head group
   // owner), b' = 0 spatial / 1 full sequence (branch-major, so each branch's
@@ -44,6 +47,13 @@ struct QkvScatter {
   int32_t Hg;
   int64_t send_rows;  // local rows M_r
   __nv_bfloat16* send;
+  // mode 1: self_g = this rank's own head group + 1 (0: every group is
+  // sent). The own group is not sent: its q, k, V^T go straight into the
+  // attention layouts sp / fs (H = Hg heads), local row m = f * Lf + l ->
+  // visual token f * Lv + self_v0 + l; send holds the other P - 1 groups in
+  // rank order.
+  int32_t self_g;
+  int32_t self_v0;
   // EPI_QKVN: RMSNorm weights [dh] per branch (0 spatial, 1 full sequence),
   // RoPE (cos, sin) tables: rope[pos_t * nt + j] (frames), then
   // rope[rope_off_y + y * ny + j] and rope[rope_off_x + x * nx + j] (patch

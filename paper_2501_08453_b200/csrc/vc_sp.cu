@@ -11,16 +11,21 @@
 // docstring).  Head group g = heads [g*H/P, (g+1)*H/P) is owned by rank g.
 //
 //   stage 1 (rank r): LN + QKV GEMM of the local rows; the epilogue writes the
-//       spatial / full-seq q, k, v straight into the a2a #1 send layout
-//       send1[g][b'][which][m][Hg][DP]; temporal branch is rank-local.
+//       spatial / full-seq q, k, v of the peers' head groups straight into the
+//       a2a #1 send layout send1[b'][g][which][m][Hg][DP] and those of the own
+//       head group straight into the attention layouts (they never travel);
+//       temporal q/k/v position-major, the temporal branch is rank-local.
 //   a2a #1 (NCCL)
-//   stage 2 (rank g): unpack into the attention layouts for the Hg heads of
-//       the group (full frames / full sequence), text K/V of the group's heads
-//       from the local prompt copy, tcgen05 attention whose epilogue writes
-//       the a2a #2 send layout send2[r][b'][m][Dg] (executor.py:395-412).
+//   stage 2 (rank g): unpack the peers' rows into the attention layouts for
+//       the Hg heads of the group, text K/V of the group's heads from the
+//       local prompt copy, tcgen05 attention whose epilogue writes the a2a #2
+//       send layout send2[b'][r][m][Dg] (executor.py:395-412) for the peers'
+//       rows and the O GEMM input for the own rows.
 //   a2a #2 (NCCL)
-//   stage 3 (rank r): gather the 2P head-group column blocks into [A_sp|A_tm|
-//       A_fs] and run the O GEMM + residual for the local rows.
+//   stage 3 (rank r): gather the peers' head-group column blocks into [A_sp|
+//       A_tm|A_fs] and run the O GEMM + residual for the local rows.
+// At one rank nothing is exchanged or unpacked: the stages are the
+// single-GPU block's kernels.
 #include <math.h>
 
 #include "vc_attn_tc.h"
@@ -43,7 +48,10 @@ struct Sp {
   int32_t vb[17];
   int64_t M[16];       // local rows F*vc_r per rank
   // exchange buffers are branch-major: [b'][peer][...]; offsets of the
-  // per-peer blocks inside one branch half, and the half sizes
+  // per-peer blocks inside one branch half, and the half sizes. The own
+  // block never enters the buffers (size 0 here): stage 1 writes the own
+  // head group's q, k, V^T straight into the attention layouts and stage 2
+  // the own rows' outputs straight into the O GEMM's input.
   int64_t s1_off[17];  // recv1 (by source rank): 3 * M_r * Hg * DP each
   int64_t s2_off[17];  // send2 (by destination rank): M_r * Dg each
   int64_t half1, half2;
@@ -89,8 +97,9 @@ int sp_make(const vc_sp_plan* pl, Sp* o, bool gather = false, bool counts_only =
   x.s1_off[0] = 0; x.s2_off[0] = 0;
   for (int r = 0; r < P; ++r) {
     x.M[r] = x.F * (x.vb[r + 1] - x.vb[r]);
-    x.s1_off[r + 1] = x.s1_off[r] + 3 * x.M[r] * x.Hg * x.DP;
-    x.s2_off[r + 1] = x.s2_off[r] + x.M[r] * x.Dg;
+    const int64_t remote = r != x.rank;
+    x.s1_off[r + 1] = x.s1_off[r] + remote * 3 * x.M[r] * x.Hg * x.DP;
+    x.s2_off[r + 1] = x.s2_off[r] + remote * x.M[r] * x.Dg;
   }
   x.half1 = x.s1_off[P];
   x.half2 = x.s2_off[P];
@@ -220,21 +229,21 @@ __global__ void __launch_bounds__(256) sp_unpack1_kernel(UnpackArgs a) {
   }
 }
 
-// recv2[b'][g][m][Dg] -> acat[m][b'*2BW + g*Dg + c]  (b'=0 spatial cols [0,BW), b'=1 full-seq [2BW,3BW);
+// recv2[b'][g][m][Dg] (g over the peers) -> acat[m][b'*2BW + g*Dg + c]  (b'=0 spatial cols [0,BW), b'=1 full-seq [2BW,3BW);
 // BW = D, or H*S with head slots)
 // One warp per (b', g, m) row, lanes across the row: 16-byte words when Dg and
 // D are multiples of 8 (every row then starts 16-byte aligned), else 4-byte.
 __global__ void __launch_bounds__(256) sp_unpack2_kernel(const __nv_bfloat16* __restrict__ recv,
-                                                         __nv_bfloat16* __restrict__ acat, int P, int64_t Mr,
-                                                         int64_t Dg, int64_t D) {  // D: branch width BW
+                                                         __nv_bfloat16* __restrict__ acat, int P, int self,
+                                                         int64_t Mr, int64_t Dg, int64_t D) {  // D: branch width BW
   const int lane = threadIdx.x & 31;
-  const int64_t rows = (int64_t)P * 2 * Mr;
+  const int64_t rows = (int64_t)P * 2 * Mr;  // P: the peers in recv2 (own group not in it)
   const bool v16 = (Dg % 8) == 0 && (D % 8) == 0;
   for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows;
        row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t m = row % Mr;
-    const int64_t gb = row / Mr;  // b'*P + g
-    const int bp = (int)(gb / P), g = (int)(gb % P);
+    const int64_t gb = row / Mr;  // b'*P + g' (g' skips the own group)
+    const int bp = (int)(gb / P), gs = (int)(gb % P), g = gs + (gs >= self);
     const __nv_bfloat16* src = recv + row * Dg;
     __nv_bfloat16* dst = acat + m * 3 * D + bp * 2 * D + (int64_t)g * Dg;
     if (v16) {
@@ -440,6 +449,7 @@ int64_t vc_sp_exchange_elems(const vc_sp_plan* plan, int32_t which, int32_t peer
   Sp x;
   if (sp_make(plan, &x, false, which >= 4) != VC_OK || peer < 0 || peer >= x.P) return -1;
   const int64_t me = x.M[x.rank];
+  if (which < 4 && peer == x.rank) return 0;  // the own block stays on the rank (sp_make)
   switch (which) {
     case 0: return 6 * me * x.Hg * x.DP;           // send1 to peer (my rows, peer's heads)
     case 1: return 6 * x.M[peer] * x.Hg * x.DP;    // recv1 from peer (peer's rows, my heads)
@@ -547,13 +557,17 @@ int vc_sp_stage1_part(const vc_sp_plan* plan, const void* packed, const float* x
     QkvScatter& s = g.qkv;
     s.pad = x.pad; s.D = x.D; s.Lv = x.Lv; s.Lt = x.Lt; s.H = (int)x.H; s.tm = tm;
     s.mode = 1; s.Hg = (int)x.Hg; s.send_rows = Mr; s.send = (bf*)send1;
+    s.Lf = vc; s.tm_F = (int)x.F;  // temporal q/k/v position-major over the local positions
+    s.self_g = (int)x.rank + 1; s.self_v0 = x.vb[x.rank];
+    s.sp = BranchOut{(bf*)(W + w.qsp), (bf*)(W + w.ksp), (bf*)(W + w.vtsp), x.Lv_ld};
+    s.fs = BranchOut{(bf*)(W + w.qfs), (bf*)(W + w.kfs), (bf*)(W + w.vtfs), x.Lk_ld};
     VC_TRY(launch_gemm_tc(xhat, x.D, pp.wqkv, x.D, g, EPI_QKV, st));
     profile_mark(st, "sp_qkv_gemm");
   }
   if (Mr > 0 && part != 0) {
     // temporal branch is rank-local: sequence = local position, tokens = frames (stride vc)
     VC_TRY(launch_temporal_bf16(tm, 3 * x.D, x.D, acat + x.BW, 3 * x.BW, (int)x.F, vc, (int)x.H, (int)x.dh, st,
-                               (int)x.S));
+                               (int)x.S, 1));
     profile_mark(st, "sp_attn_temporal");
   }
   profile_end();
@@ -583,14 +597,16 @@ int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed, const void* 
     a.Hg = (int)x.Hg; a.DP = (int)x.DP; a.branch = branch;
     a.groups[0] = 0;
     for (int r = 0; r <= x.P; ++r) { a.vb[r] = x.vb[r]; a.off[r] = x.s1_off[r]; }
-    for (int r = 0; r < x.P; ++r) a.groups[r + 1] = a.groups[r] + 3 * cdiv(x.M[r], 32);
+    for (int r = 0; r < x.P; ++r) a.groups[r + 1] = a.groups[r] + (r == x.rank ? 0 : 3 * cdiv(x.M[r], 32));
     a.qsp = sp.q; a.ksp = sp.k; a.vtsp = sp.vt; a.qfs = fs.q; a.kfs = fs.k; a.vtfs = fs.vt;
     a.Lv_ld = x.Lv_ld; a.Lk_ld = x.Lk_ld;
     const int64_t warps = a.groups[x.P];
     const int blocks = (int)std::min<int64_t>(cdiv(warps, 8), 148 * 8);
-    if (blocks > 0) sp_unpack1_kernel<<<blocks, 256, 0, st>>>(a);
-    VC_CHECK_LAUNCH();
-    profile_mark(st, branch == 0 ? "sp_unpack1_spatial" : "sp_unpack1_fullseq");
+    if (blocks > 0) {  // the peers' rows (the own ones were written by stage 1)
+      sp_unpack1_kernel<<<blocks, 256, 0, st>>>(a);
+      VC_CHECK_LAUNCH();
+      profile_mark(st, branch == 0 ? "sp_unpack1_spatial" : "sp_unpack1_fullseq");
+    }
   }
   const int g = (int)x.rank;
   if (branch == 1 && x.Lt > 0) {  // text K, V of this head group from the local prompt copy
@@ -612,6 +628,9 @@ int vc_sp_stage2_branch(const vc_sp_plan* plan, const void* packed, const void* 
   a.spo.P = (int)x.P; a.spo.branch = branch; a.spo.F = (int)x.F; a.spo.Lv = (int)x.Lv; a.spo.Dg = x.Dg;
   a.head_slot = (int)x.S;
   for (int r = 0; r <= x.P; ++r) { a.spo.vb[r] = x.vb[r]; a.spo.base[r] = branch * x.half2 + x.s2_off[r]; }
+  a.spo.self_r1 = (int)x.rank + 1;  // own rows: straight into acat (branch b' columns b'*2BW + g*Dg)
+  a.spo.self_out = (bf*)(W + w.acat) + branch * 2 * x.BW + g * x.Dg;
+  a.spo.self_ld = 3 * x.BW;
   if (branch == 0) {
     a.Lq = (int)x.Lv; a.Lk = (int)x.Lv; a.n_bias = 0; a.bias_log2 = 0.f;
     VC_TRY(launch_attn_tc(a, sp.q, sp.k, sp.vt, (int)x.F, x.Lv, x.Lv, x.Lv_ld, (int)x.DP, st));
@@ -644,10 +663,10 @@ int vc_sp_stage3(const vc_sp_plan* plan, const void* packed, const void* recv2, 
   const int64_t Mr = x.M[x.rank];
   if (Mr == 0) return VC_OK;
   bf* acat = (bf*)((char*)ws + w.acat);
-  {
-    const int64_t rows = x.P * 2 * Mr;  // one warp per row
+  if (x.P > 1) {  // the peers' head groups (the own one was written by stage 2)
+    const int64_t rows = (x.P - 1) * 2 * Mr;  // one warp per row
     const int blocks = (int)std::min<int64_t>(cdiv(rows, 8), 148 * 16);
-    sp_unpack2_kernel<<<blocks, 256, 0, st>>>((const bf*)recv2, acat, (int)x.P, Mr, x.Dg, x.BW);
+    sp_unpack2_kernel<<<blocks, 256, 0, st>>>((const bf*)recv2, acat, (int)x.P - 1, (int)x.rank, Mr, x.Dg, x.BW);
     VC_CHECK_LAUNCH();
     profile_mark(st, "sp_unpack2");
   }

@@ -120,7 +120,11 @@ class TorchExchange:
 
     def all_to_all(self, recv, send, recv_counts, send_counts, async_op=False):
         """Returns a handle with .wait() (the current stream waits for the
-        collective; NCCL runs it on its own stream) when async_op."""
+        collective; NCCL runs it on its own stream) when async_op. Nothing
+        to move (one rank: the own block never enters the buffers) is no
+        collective at all."""
+        if len(send_counts) == 1 and not send_counts[0] and not recv_counts[0]:
+            return _Done() if async_op else None
         return self.dist.all_to_all_single(recv, send, recv_counts, send_counts, group=self.group,
                                            async_op=async_op)
 
@@ -130,12 +134,18 @@ class TorchExchange:
         self.dist.all_gather_into_tensor(gather, gather[rank * n:(rank + 1) * n], group=self.group)
 
 
+class _Done:
+    def wait(self):
+        return None
+
+
 @dataclass(frozen=True)
 class CommEvent:
     """One collective this rank issued (executor.py:91-108's CommEvent fields;
-    bytes_per_device is what this rank hands to the collective, its own
-    block included, as laid out; payload_bytes the same exchange without
-    the layout padding, in the reference's payload terms)."""
+    bytes_per_device is what this rank hands to the collective as laid out
+    (its own block excluded: it never leaves the rank); payload_bytes the
+    same exchange in the reference's payload terms: no layout padding, own
+    block included, as the reference's executor logs it)."""
     stage: str
     collective: str
     group_size: int
@@ -191,10 +201,13 @@ class SPBlock:
 
     def launches_per_forward(self) -> int:
         """Kernels this rank launches per forward (vc_sp.cu; NCCL's own not counted):
-        stage 1 LN + QKV GEMM + temporal, stage 2 unpack + text K/V GEMMs (2) +
-        spatial + full-sequence attention, stage 3 unpack + O GEMM."""
+        stage 1 LN + QKV GEMM + temporal, stage 2 per branch an unpack of the
+        peers' rows (P > 1) + text K/V GEMMs (2) + spatial + full-sequence
+        attention, stage 3 unpack of the peers' groups (P > 1) + O GEMM."""
         mr = self.F * (self.vb[self.rank + 1] - self.vb[self.rank])
-        return (3 if mr > 0 else 1) + 1 + (2 if self.Lt > 0 else 0) + 2 + (2 if mr > 0 else 0)
+        peers = self.P > 1
+        return ((3 if mr > 0 else 1) + (2 if peers else 0) + (2 if self.Lt > 0 else 0) + 2
+                + ((2 if peers else 1) if mr > 0 else 0))
 
     def __init__(self, torch, device_block, frames, visual_len, text_len, nranks, rank):
         if device_block.dtype != "bf16":
@@ -751,13 +764,14 @@ def bench_sp(args, torch, world, rank, local, CONFIGS, METRIC, algorithmic_flops
             # bytes leaving this rank over NVLink (its own block stays local)
             wire = 2 * (sum(bc[tag]) - bc[tag][rank])
             alg = 2 * (sum(ref[tag]) - ref[tag][rank])
-            a2a[k] = {"ms": ms_k, "nvlink_bytes_per_rank": wire, "nvlink_gbs": wire / (ms_k / 1e3) / 1e9,
-                      "algorithmic_bytes_per_rank": alg,
-                      "algorithmic_gbs": alg / (ms_k / 1e3) / 1e9}
+            gbs = (lambda b: b / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0)  # noqa: E731
+            a2a[k] = {"ms": ms_k, "nvlink_bytes_per_rank": wire, "nvlink_gbs": gbs(wire),
+                      "algorithmic_bytes_per_rank": alg, "algorithmic_gbs": gbs(alg)}
         a2a["note"] = ("each all-to-all timed alone (blocking, CUDA events, max over ranks); in the block "
                        "step they overlap attention (sp.run_stages). nvlink_bytes = what this rank sends to "
                        "its peers as laid out (head dim padded 66 -> 80); algorithmic = the reference's "
-                       "payload (executor.py:344-347, :395-412). At 1 rank every exchange is a local copy.")
+                       "payload (executor.py:344-347, :395-412). The own block never enters the exchange buffers "
+                       "(stage 1 / 2 write it where stage 2 / 3 read it): at 1 rank there is no collective.")
     else:  # bf16 bytes sent per rank: own slot to every peer
         a2a["bytes_sent_per_rank_per_step"] = 2 * spb.slot * (world - 1)
     flops = sum(algorithmic_flops(F, Lv, Lt, D, H).values())

@@ -7,7 +7,9 @@ same exchange buffer layouts as paper_2501_08453_b200/csrc/vc_sp.cu:
   send2 (rank g) [b'][r][M_r][Dg]
   recv2 (rank r) [b'][g][M_r][Dg]
 
-(branch-major, so the product's driver runs one all-to-all per branch)
+(branch-major, so the product's driver runs one all-to-all per branch; the
+peer index runs over the OTHER ranks: the own block stays local, in
+local1 / local2 here, as the product writes it straight where it is read)
 
 so the real torch.distributed all_to_all_single (gloo here, NCCL on the GPU
 box) is exercised with the exact per-peer counts of the product
@@ -32,6 +34,7 @@ class NumpyStages:
         self.payload_counts = sp.exchange_counts(F, Lv, H, D, P, rank, padded=False)
         mk = lambda k: torch.zeros(sum(self.counts[k]), dtype=torch.float64)  # noqa: E731
         self.send1, self.recv1, self.send2, self.recv2 = mk("send1"), mk("recv1"), mk("send2"), mk("recv2")
+        self.peers = [r for r in range(P) if r != rank]
 
     # stage 1: local rows -> q/k/v by head group + local temporal branch
     def stage1(self, x_local, prompt, part=2):
@@ -42,12 +45,14 @@ class NumpyStages:
         vc = xl.shape[1]
         rows = xl.reshape(-1, D)
         Mr = rows.shape[0]
-        s1 = self.send1.numpy().reshape(2, self.P, 3, Mr, Hg, DP)
+        s1 = self.send1.numpy().reshape(2, self.P - 1, 3, Mr, Hg, DP)
+        self.local1 = np.zeros((2, 3, Mr, Hg, DP))
         for bp, params in enumerate((self.block.spatial, self.block.fullseq)):
             for which, t in enumerate(O.branch_qkv(params, rows)):
                 th = t.reshape(Mr, self.H, dh)
                 for g in range(self.P):
-                    s1[bp, g, which, :, :, :dh] = th[:, g * Hg:(g + 1) * Hg]
+                    dst = self.local1[bp] if g == self.rank else s1[bp, self.peers.index(g)]
+                    dst[which, :, :, :dh] = th[:, g * Hg:(g + 1) * Hg]
         q, k, v = O.branch_qkv(self.block.temporal, rows)
         tr = lambda a: a.reshape(F, vc, D).transpose(1, 0, 2)  # noqa: E731  [vc, F, D]
         self.a_tm = O.attention(tr(q), tr(k), tr(v), self.H).transpose(1, 0, 2).reshape(Mr, D)
@@ -63,9 +68,12 @@ class NumpyStages:
         off = branch * (r1.size // 2)
         for r in range(P):
             vc, Mr = self.vb[r + 1] - self.vb[r], self.M[r]
-            blk = r1[off:off + 3 * Mr * Hg * DP].reshape(3, F, vc, Hg, DP)[..., :dh]
+            if r == g:
+                blk = self.local1[branch].reshape(3, F, vc, Hg, DP)[..., :dh]
+            else:
+                blk = r1[off:off + 3 * Mr * Hg * DP].reshape(3, F, vc, Hg, DP)[..., :dh]
+                off += 3 * Mr * Hg * DP
             full[:, :, self.vb[r]:self.vb[r + 1]] = blk.reshape(3, F, vc, Hg * dh)
-            off += 3 * Mr * Hg * DP
         if branch == 0:
             out = O.attention(full[0], full[1], full[2], Hg)            # [F, Lv, Hg*dh]
         else:
@@ -77,8 +85,13 @@ class NumpyStages:
             out = O.attention(full[0].reshape(Nv, -1), K, V, Hg, w).reshape(F, Lv, -1)
         s2 = self.send2.numpy()
         off = branch * (s2.size // 2)
+        if branch == 0:
+            self.local2 = np.zeros((2, self.M[g], self.Dg))
         for r in range(P):
             Mr = self.M[r]
+            if r == g:
+                self.local2[branch] = out[:, self.vb[r]:self.vb[r + 1]].reshape(Mr, self.Dg)
+                continue
             s2[off:off + Mr * self.Dg].reshape(F, -1, self.Dg)[:] = out[:, self.vb[r]:self.vb[r + 1]]
             off += Mr * self.Dg
 
@@ -88,10 +101,11 @@ class NumpyStages:
         Mr = self.M[self.rank]
         acat = np.zeros((Mr, 3 * D))
         acat[:, D:2 * D] = self.a_tm
-        r2 = self.recv2.numpy().reshape(2, P, Mr, Dg)
+        r2 = self.recv2.numpy().reshape(2, P - 1, Mr, Dg)
         for g in range(P):
-            acat[:, g * Dg:(g + 1) * Dg] = r2[0, g]
-            acat[:, 2 * D + g * Dg:2 * D + (g + 1) * Dg] = r2[1, g]
+            blk = self.local2 if g == self.rank else r2[:, self.peers.index(g)]
+            acat[:, g * Dg:(g + 1) * Dg] = blk[0]
+            acat[:, 2 * D + g * Dg:2 * D + (g + 1) * Dg] = blk[1]
         W = np.concatenate([self.block.spatial.wo, self.block.temporal.wo, self.block.fullseq.wo])
         y = (acat @ W).reshape(x_local.shape)
         if add_residual:

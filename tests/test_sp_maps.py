@@ -51,14 +51,16 @@ def test_cabi_bounds_and_counts_closed_form(P):
         assert lib.vc_sp_bounds(C.byref(plan), cvb) == 0
         assert list(cvb) == vb
         got = sp.exchange_counts(F, Lv, H, D, P, rank)
-        assert got["send1"] == [6 * M[rank] * Hg * DP] * P
-        assert got["recv1"] == [6 * M[r] * Hg * DP for r in range(P)]
-        assert got["send2"] == [2 * M[r] * Hg * DP for r in range(P)]
-        assert got["recv2"] == [2 * M[rank] * Hg * DP] * P
-        ref = sp.exchange_counts(F, Lv, H, D, P, rank, padded=False)
+        peer = [int(r != rank) for r in range(P)]  # the own block never enters the buffers
+        assert got["send1"] == [6 * M[rank] * Hg * DP * peer[r] for r in range(P)]
+        assert got["recv1"] == [6 * M[r] * Hg * DP * peer[r] for r in range(P)]
+        assert got["send2"] == [2 * M[r] * Hg * DP * peer[r] for r in range(P)]
+        assert got["recv2"] == [2 * M[rank] * Hg * DP * peer[r] for r in range(P)]
+        ref = sp.exchange_counts(F, Lv, H, D, P, rank, padded=False)  # the reference's payload: own block in
         assert ref["send1"] == [6 * M[rank] * Hg * dh] * P
         assert ref["send2"] == [2 * M[r] * Hg * dh for r in range(P)]
-        assert sum(got["send2"]) * dh == sum(ref["send2"]) * DP  # the 80/66 head-slot inflation
+        own = ref["send2"][rank]
+        assert sum(got["send2"]) * dh == (sum(ref["send2"]) - own) * DP  # the 80/66 head-slot inflation
         assert lib.vc_sp_workspace_bytes(C.byref(plan)) > 0
 
 
