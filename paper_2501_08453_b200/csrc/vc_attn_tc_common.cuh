@@ -84,17 +84,20 @@ __device__ __forceinline__ float softmax_step(float (&v)[BKV], int k0, const Att
   return alpha;
 }
 
-// O (TMEM, DP fp32 columns of this lane) *= alpha
-template <int DP, int C0 = 0, int C1 = DP / 16>
+// O (TMEM, DP fp32 columns of this lane) *= alpha; ON < DP: O holds only
+// ON columns (the last 16-column chunk is ON % 16 = 8 wide)
+template <int DP, int C0 = 0, int C1 = DP / 16, int ON = DP>
 __device__ __forceinline__ void rescale_o(uint32_t o_addr, float alpha) {
 #pragma unroll
   for (int c = C0; c < C1; ++c) {
     uint32_t r[16];
-    ptx::tmem_ld16(o_addr + c * 16, r);
+    if (c * 16 + 16 <= ON) ptx::tmem_ld16(o_addr + c * 16, r);
+    else ptx::tmem_ld8p(o_addr + c * 16, r);
     ptx::tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-    ptx::tmem_st16(o_addr + c * 16, r);
+    if (c * 16 + 16 <= ON) ptx::tmem_st16(o_addr + c * 16, r);
+    else ptx::tmem_st8p(o_addr + c * 16, r);
   }
   ptx::tmem_st_wait();
 }
@@ -135,7 +138,7 @@ __device__ __forceinline__ __nv_bfloat16* out_row(const AttnTcParams& p, int qi,
          (int64_t)h * (p.head_slot ? p.head_slot : p.dh);
 }
 
-template <int DP, int C0 = 0, int C1 = DP / 16>
+template <int DP, int C0 = 0, int C1 = DP / 16, int ON = DP>
 __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr, float l, int qi, int seq,
                                           int h) {
   const float inv = 1.f / l;
@@ -144,7 +147,13 @@ __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr
 #pragma unroll
     for (int c = C0; c < C1; ++c) {
       uint32_t r[16];
-      ptx::tmem_ld16(o_addr + c * 16, r);
+      if (c * 16 + 16 <= ON) {
+        ptx::tmem_ld16(o_addr + c * 16, r);
+      } else {  // O holds ON = 16c + 8 columns: the rest are past dh (zero in the slot)
+        ptx::tmem_ld8p(o_addr + c * 16, r);
+#pragma unroll
+        for (int i = 8; i < 16; ++i) r[i] = 0u;
+      }
       ptx::tmem_ld_wait();
       if (orow) {
         uint32_t w[8];
@@ -168,7 +177,13 @@ __device__ __forceinline__ void store_out(const AttnTcParams& p, uint32_t o_addr
 #pragma unroll
   for (int c = C0; c < C1; ++c) {
     uint32_t r[16];
-    ptx::tmem_ld16(o_addr + c * 16, r);
+    if (c * 16 + 16 <= ON) {
+      ptx::tmem_ld16(o_addr + c * 16, r);
+    } else {
+      ptx::tmem_ld8p(o_addr + c * 16, r);
+#pragma unroll
+      for (int i = 8; i < 16; ++i) r[i] = 0u;
+    }
     ptx::tmem_ld_wait();
     if (orow) {
 #pragma unroll

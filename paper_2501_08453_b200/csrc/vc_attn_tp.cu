@@ -42,7 +42,23 @@ __device__ unsigned long long g_attn_tracep[18][256][8];
   do {                                                                       \
     if ((cond) && (j) < 256) g_attn_tracep[role][j][k] = clock64();         \
   } while (0)
+// per-CTA timeline: clock64 at entry, first S seen, last P.V done, output
+// stored (after the final barrier), then %smid (tools/attn_trace.cu: per-SM gaps)
+__device__ unsigned long long g_attn_cta[16384][5];
+#define VC_CTA(slot)                                                                                \
+  do {                                                                                              \
+    const unsigned b_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);          \
+    if (b_ < 16384) g_attn_cta[b_][slot] = clock64();                                              \
+    if ((slot) == 0 && b_ < 16384) {                                                                \
+      unsigned sm_;                                                                                 \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                                              \
+      g_attn_cta[b_][4] = sm_;                                                                      \
+    }                                                                                               \
+  } while (0)
 #else
+#define VC_CTA(slot) \
+  do {               \
+  } while (0)
 #define VC_TRP(cond, role, j, k) \
   do {                           \
   } while (0)
@@ -57,16 +73,23 @@ __device__ unsigned long long g_attn_tracep[18][256][8];
 constexpr int kWarpsTp = 19;
 constexpr int kThreadsTp = kWarpsTp * 32;
 
-template <int DP>
+// NARROW (DP 80, dh <= 71): 120-key blocks with O in 72 columns (dh + the
+// ones column): S 120 + P 64 + O 72 = 256. P.V runs over 128 keys (P zero for
+// keys 120..127) with N = 72; M = 128 MMAs with N % 16 == 8 are exact
+// (tools/mma_mn_test.cu case 5). 1350 keys take 12 blocks instead of 13.
+template <int DP, bool NARROW = false>
 struct CfgTp {
   static constexpr int N64 = DP / 64;
   static constexpr int TAIL = DP % 64;
   static_assert(TAIL == 0 || TAIL == 16, "DP must be 64*n or 64*n+16");
   static_assert(DP <= 80, "S + P + O must fit 256 TMEM columns per tile");
-  static constexpr int BK = DP == 64 ? 128 : 112;  // keys per block
-  static constexpr int HK = BK / 2;                // keys per softmax half
-  static constexpr int SCOL = 0, PCOL = BK, OCOL = BK + BK / 2;
-  static_assert(OCOL + DP <= 256, "per-tile TMEM columns");
+  static_assert(!NARROW || DP == 80, "the narrow layout is the DP 80 one");
+  static constexpr int BK = NARROW ? 120 : DP == 64 ? 128 : 112;  // keys per block
+  static constexpr int HK = BK / 2;                               // keys per softmax half
+  static constexpr int PKEYS = NARROW ? 128 : BK;                 // the P.V K extent
+  static constexpr int ON = NARROW ? 72 : DP;                     // O columns
+  static constexpr int SCOL = 0, PCOL = BK, OCOL = BK + PKEYS / 2;
+  static_assert(OCOL + ON <= 256, "per-tile TMEM columns");
   static constexpr int Q_BYTES = BQ * DP * 2;
   static constexpr int K_BYTES = BK * DP * 2;
   static constexpr int K_STAGE = (K_BYTES + 1023) / 1024 * 1024;  // SW128 tiles start 1024-aligned
@@ -79,17 +102,17 @@ struct CfgTp {
   static constexpr int OFF_BAR = OFF_X + 2 * 2 * 2 * BQ * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int KSTEPS = DP / 16;
-  static constexpr int NC = DP / 16;
+  static constexpr int NC = (ON + 15) / 16;
   static constexpr int NC0 = (NC + 1) / 2;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, int POLY, bool ONES>
+template <int DP, int POLY, bool ONES, bool NARROW>
 __global__ void __launch_bounds__(kThreadsTp, 1)
     attn_tp_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
                    const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
-  using CF = CfgTp<DP>;
+  using CF = CfgTp<DP, NARROW>;
   constexpr int KS = CF::KS, BK = CF::BK, HK = CF::HK;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -112,6 +135,7 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
   const int n_tiles = (p.Lk + BK - 1) / BK;
   const int ntile = q0 + BQ < p.Lq ? 2 : 1;  // the last CTA of a sequence may hold one tile
   [[maybe_unused]] const bool tr = blockIdx.x == min(20u, gridDim.x - 1) && blockIdx.y == 3 && blockIdx.z == 0;
+  if (threadIdx.x == 0) VC_CTA(0);
 
   if (warp == 0 && ptx::elect_one()) {
     ptx::prefetch_tmap(&tmQ64); ptx::prefetch_tmap(&tmK64); ptx::prefetch_tmap(&tmV);
@@ -177,7 +201,7 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
     const int t = warp - 1;
     if (t < ntile) {
       constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BK);
-      constexpr uint32_t idO = ptx::idesc_bf16_f32(BQ, DP);
+      constexpr uint32_t idO = ptx::idesc_bf16_f32(BQ, CF::ON);
       const uint32_t sQ = ptx::smem_u32(smem + CF::OFF_Q + t * CF::Q_BYTES), sK = ptx::smem_u32(smem + CF::OFF_K),
                      sV = ptx::smem_u32(smem + CF::OFF_V);
       const uint64_t dQ = ptx::smem_desc(sQ, 0, 1024, ptx::kLayoutSW128);
@@ -201,7 +225,7 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
       auto mma_pv = [&](int ks, int j) {  // O_t += P_t V(ks)
         const uint64_t vo = (uint64_t)((ks * CF::V_BYTES) >> 4);
 #pragma unroll
-        for (int c = 0; c < BK / 16; ++c)
+        for (int c = 0; c < CF::PKEYS / 16; ++c)
           ptx::mma_bf16_ts(tOd, tPa + 8 * c, dV + vo + (uint64_t)(((c >> 2) * DP * 128 + (c & 3) * 32) >> 4), idO,
                            (j > 0 || c > 0) ? 1u : 0u);
         ptx::mma_commit(&pv_done[t]);
@@ -248,6 +272,13 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
     const uint32_t bar_id = 1 + t * 4 + quarter;
     const bool trs = tr && lane == 0;
     if (t < ntile) {
+      if constexpr (CF::PKEYS > BK) {  // P of keys BK..PKEYS-1 stays zero (written once)
+        if (half == 1) {
+          const uint32_t z[(CF::PKEYS - BK) / 2] = {};
+          ptx::tmem_st_cols<0, (CF::PKEYS - BK) / 2>(tmem + t * 256 + lane_off + CF::PCOL + BK / 2, z);
+          ptx::tmem_st_wait();
+        }
+      }
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
         const int kt = j * BK;
@@ -256,6 +287,7 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
         VC_SM_WAIT(&s_full[t], j & 1);
         ptx::fence_after_sync();
         VC_TRP(trs, 2 + sw, j, 0);
+        if (j == 0 && sw == 0 && lane == 0) VC_CTA(1);
         uint32_t r[HK];
         // 32 / 16 / 8-column pieces (half 1 starts at column 56: the loads
         // need no 32-column alignment; 7 x8 loads measured 2% slower)
@@ -320,8 +352,8 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
         VC_TRP(trs, 2 + sw, j, 3);
         ptx::tmem_st_cols<0, HK / 2>(tP, pk);  // 16 / 8 / 4-column pieces (x4 only: 2% slower)
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          if (half == 0) rescale_o<DP, 0, CF::NC0>(tO, alpha);
-          else rescale_o<DP, CF::NC0, CF::NC>(tO, alpha);
+          if (half == 0) rescale_o<DP, 0, CF::NC0, CF::ON>(tO, alpha);
+          else rescale_o<DP, CF::NC0, CF::NC, CF::ON>(tO, alpha);
         }
         ptx::tmem_st_wait();
         ptx::fence_before_sync();
@@ -330,6 +362,7 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
       }
       VC_SM_WAIT(&pv_done[t], (n_tiles - 1) & 1);
       ptx::fence_after_sync();
+      if (sw == 0 && lane == 0) VC_CTA(2);
       if (ONES) {  // row sum accumulated by the tensor core in the ones column
         uint32_t r1;
         ptx::tmem_ld1(tO + p.dh, r1);
@@ -341,12 +374,13 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
         ptx::named_bar_sync(bar_id, 64);
         l += xj[(half ^ 1) * BQ + row];
       }
-      if (half == 0) store_out<DP, 0, CF::NC0>(p, tO, l, q0 + t * BQ + row, seq, h);
-      else store_out<DP, CF::NC0, CF::NC>(p, tO, l, q0 + t * BQ + row, seq, h);
+      if (half == 0) store_out<DP, 0, CF::NC0, CF::ON>(p, tO, l, q0 + t * BQ + row, seq, h);
+      else store_out<DP, CF::NC0, CF::NC, CF::ON>(p, tO, l, q0 + t * BQ + row, seq, h);
     }
   }
   ptx::fence_before_sync();
   __syncthreads();
+  if (threadIdx.x == 0) VC_CTA(3);
   if (warp == 1) {
     ptx::fence_after_sync();
     ptx::tmem_dealloc(tmem, 512);
@@ -359,26 +393,54 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
 int attn_tracep_read(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, g_attn_tracep, sizeof(g_attn_tracep)) == cudaSuccess ? 0 : -1;
 }
+int attn_cta_read(unsigned long long* host) {  // [16384][5]
+  return cudaMemcpyFromSymbol(host, g_attn_cta, sizeof(g_attn_cta)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
+#ifdef VC_TUNING
+// measured-and-dropped variant (profiles/r02/attn/README.md): tuning builds only
+static int launch_attn_tp_narrow(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
+                                 int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
+  using CF = CfgTp<80, true>;
+  AttnMaps m;
+  VC_TRY((make_attn_maps<80, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
+  static bool attr = false;
+  if (!attr) {
+    VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<80, 4, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       CF::SMEM));
+    attr = true;
+  }
+  dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
+  attn_tp_kernel<80, 4, true, true><<<grid, kThreadsTp, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);
+  VC_CHECK_LAUNCH();
+  return VC_OK;
+}
 #endif
 
 template <int DP>
 int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
+  const bool ones = p.dh < DP;
+#ifdef VC_TUNING
+  static const int narrow_on = tuning_int("VC_ATTN_NARROW", 0);
+  if (DP == 80 && ones && p.dh < 72 && narrow_on) return launch_attn_tp_narrow(p, q, k, vt, nseq, q_rows_per_seq,
+                                                                           k_rows_per_seq, ld_key, st);
+#endif
   using CF = CfgTp<DP>;
   AttnMaps m;
   VC_TRY((make_attn_maps<DP, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
-  const bool ones = p.dh < DP;
   static const int poly = tuning_int("VC_POLY_EVERY", 4);
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
 #define VC_ATTN_TP_CASE(PV, ON)                                                                                  \
   if (poly == PV && ones == ON) {                                                                               \
     static bool attr = false;                                                                                   \
     if (!attr) {                                                                                                \
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, PV, ON>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, PV, ON, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                          CF::SMEM));                                                            \
       attr = true;                                                                                              \
     }                                                                                                           \
-    attn_tp_kernel<DP, PV, ON><<<grid, kThreadsTp, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);         \
+    attn_tp_kernel<DP, PV, ON, false><<<grid, kThreadsTp, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);  \
     VC_CHECK_LAUNCH();                                                                                          \
     return VC_OK;                                                                                               \
   }

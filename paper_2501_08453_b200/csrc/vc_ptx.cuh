@@ -323,6 +323,9 @@ __device__ __forceinline__ void tmem_st4p(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
                "r"(r[2]), "r"(r[3]));
 }
+__device__ __forceinline__ void tmem_st2p(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(r[0]), "r"(r[1]));
+}
 __device__ __forceinline__ void tmem_ld4p(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -364,8 +367,11 @@ __device__ __forceinline__ void tmem_st_cols(uint32_t base, const uint32_t* r) {
     static_assert(C % 4 == 0, "tmem_st_cols: 4-column granularity");
     tmem_st4p(base + C, r);
     tmem_st_cols<C + 4, N - 4>(base, r + 4);
+  } else if constexpr (N >= 2) {
+    tmem_st2p(base + C, r);
+    tmem_st_cols<C + 2, N - 2>(base, r + 2);
   } else {
-    static_assert(N == 0, "tmem_st_cols: N multiple of 4");
+    static_assert(N == 0, "tmem_st_cols: N multiple of 2");
   }
 }
 __device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t r) {

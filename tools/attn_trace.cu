@@ -6,6 +6,7 @@
 //   attn_trace [Lq Lk H dh n_bias reps]   -> kernel ms, TFLOP/s, trace CSV on stdout
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 
 #include <cuda_bf16.h>
@@ -16,6 +17,7 @@
 namespace vc {
 int attn_trace3_read(unsigned long long* host);
 int attn_tracep_read(unsigned long long* host);
+int attn_cta_read(unsigned long long* host);
 }
 
 __global__ void fill_kernel(__nv_bfloat16* x, size_t n, uint32_t seed, float amp) {
@@ -46,6 +48,7 @@ int main(int argc, char** argv) {
   p.Lq = Lq; p.Lk = Lk; p.H = H; p.dh = dh; p.n_bias = n_bias;
   p.bias_log2 = 2.f; p.scale_log2 = 1.4426950408889634f / sqrtf((float)dh);
   p.out = getenv("VC_TRACE_NO_OUT") ? nullptr : out; p.ld_out = getenv("VC_TRACE_LD80") ? (int64_t)H * 80 : (int64_t)H * dh; p.col_off = 0; p.out_seq_rows = Lq;
+  if (getenv("VC_TRACE_SLOT")) { p.head_slot = 80; p.ld_out = (int64_t)H * 80; }  // the block's layout: 80-column head slots
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   int rc = vc::launch_attn_tc(p, q, k, vt, 1, Lq, Lk, ld_key, DP, 0);
@@ -62,6 +65,26 @@ int main(int argc, char** argv) {
   const double flop = 4.0 * Lq * (double)Lk * H * dh;
   printf("# Lq %d Lk %d H %d dh %d DP %d: %.4f ms  %.1f TFLOP/s (algorithmic dh)\n", Lq, Lk, H, dh, DP, ms,
          flop / ms / 1e9);
+  if (getenv("VC_TRACE_CTA")) {  // per-CTA phases of the LAST launch, per-SM gaps between CTAs
+    std::vector<unsigned long long> c(16384 * 5);
+    vc::attn_cta_read(c.data());
+    const int nb = ((Lq + 255) / 256) * H;
+    double pro = 0, main_ = 0, epi = 0, gap = 0;
+    int ng = 0, n = 0;
+    std::vector<std::vector<std::pair<unsigned long long, unsigned long long>>> sm(256);
+    for (int b = 0; b < nb && b < 16384; ++b) {
+      const unsigned long long* e = &c[b * 5];
+      if (!e[0] || !e[1] || !e[2] || !e[3]) continue;
+      pro += (double)(e[1] - e[0]); main_ += (double)(e[2] - e[1]); epi += (double)(e[3] - e[2]); ++n;
+      sm[e[4] & 255].push_back({e[0], e[3]});
+    }
+    for (auto& v : sm) {
+      std::sort(v.begin(), v.end());
+      for (size_t i = 1; i < v.size(); ++i) { gap += (double)v[i].first - (double)v[i - 1].second; ++ng; }
+    }
+    printf("# CTAs %d: clk per CTA prologue (entry -> first S) %.0f, main (-> last P.V) %.0f, epilogue (-> stored) %.0f; "
+           "mean gap between CTAs on one SM %.0f clk (%d gaps)\n", n, pro / n, main_ / n, epi / n, ng ? gap / ng : 0.0, ng);
+  }
   const int nj = 256;
   std::vector<unsigned long long> tr(18 * 512 * 8);
   const char* impl = getenv("VC_ATTN_IMPL");
