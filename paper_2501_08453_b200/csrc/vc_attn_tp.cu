@@ -70,14 +70,15 @@ __device__ unsigned long long g_attn_cta[16384][5];
 #define VC_SM_WAIT ptx::mbar_wait_sleep
 #endif
 
-constexpr int kWarpsTp = 19;
-constexpr int kThreadsTp = kWarpsTp * 32;
 
 // NARROW (DP 80, dh <= 71): 120-key blocks with O in 72 columns (dh + the
 // ones column): S 120 + P 64 + O 72 = 256. P.V runs over 128 keys (P zero for
 // keys 120..127) with N = 72; M = 128 MMAs with N % 16 == 8 are exact
 // (tools/mma_mn_test.cu case 5). 1350 keys take 12 blocks instead of 13.
-template <int DP, bool NARROW = false>
+// FR (full row): one softmax thread per query row (4 warps per tile, 12
+// warps: w0 TMA, w1 / w2 MMA issuers, w3 idle, w4..w11 softmax) instead of
+// two warps per row meeting in shared memory for the row max.
+template <int DP, bool NARROW = false, bool FR = false>
 struct CfgTp {
   static constexpr int N64 = DP / 64;
   static constexpr int TAIL = DP % 64;
@@ -85,7 +86,10 @@ struct CfgTp {
   static_assert(DP <= 80, "S + P + O must fit 256 TMEM columns per tile");
   static_assert(!NARROW || DP == 80, "the narrow layout is the DP 80 one");
   static constexpr int BK = NARROW ? 120 : DP == 64 ? 128 : 112;  // keys per block
-  static constexpr int HK = BK / 2;                               // keys per softmax half
+  static constexpr int HK = FR ? BK : BK / 2;                     // keys per softmax thread
+  static constexpr int WARPS = FR ? 12 : 19;
+  static constexpr int SM0 = FR ? 4 : 3;                          // first softmax warp
+  static constexpr int SM_ARRIVALS = FR ? 128 : 256;              // softmax threads per tile
   static constexpr int PKEYS = NARROW ? 128 : BK;                 // the P.V K extent
   static constexpr int ON = NARROW ? 72 : DP;                     // O columns
   static constexpr int SCOL = 0, PCOL = BK, OCOL = BK + PKEYS / 2;
@@ -107,12 +111,12 @@ struct CfgTp {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, int POLY, bool ONES, bool NARROW>
-__global__ void __launch_bounds__(kThreadsTp, 1)
+template <int DP, int POLY, bool ONES, bool NARROW, bool FR = false>
+__global__ void __launch_bounds__(CfgTp<DP, NARROW, FR>::WARPS * 32, 1)
     attn_tp_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
                    const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
-  using CF = CfgTp<DP, NARROW>;
+  using CF = CfgTp<DP, NARROW, FR>;
   constexpr int KS = CF::KS, BK = CF::BK, HK = CF::HK;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -149,8 +153,8 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&s_empty[t], 256);
-      ptx::mbar_init(&p_full[t], 256);
+      ptx::mbar_init(&s_empty[t], CF::SM_ARRIVALS);
+      ptx::mbar_init(&p_full[t], CF::SM_ARRIVALS);
       ptx::mbar_init(&pv_done[t], 1);
     }
     ptx::fence_barrier_init();
@@ -256,11 +260,11 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
         VC_TRP(tr && (threadIdx.x & 31) == 0, t, j, 2);
       }
     }
-  } else {
+  } else if (warp >= CF::SM0) {
     // ===================== softmax (tile t, key half), correction, epilogue =====================
-    const int sw = warp - 3;
-    const int t = sw >> 3;
-    const int half = (sw >> 2) & 1;
+    const int sw = warp - CF::SM0;
+    const int t = FR ? sw >> 2 : sw >> 3;
+    const int half = FR ? 0 : (sw >> 2) & 1;
     const int quarter = warp & 3;
     const int lane = threadIdx.x & 31;
     const int row = quarter * 32 + lane;
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
     const bool trs = tr && lane == 0;
     if (t < ntile) {
       if constexpr (CF::PKEYS > BK) {  // P of keys BK..PKEYS-1 stays zero (written once)
-        if (half == 1) {
+        if (half == (FR ? 0 : 1)) {
           const uint32_t z[(CF::PKEYS - BK) / 2] = {};
           ptx::tmem_st_cols<0, (CF::PKEYS - BK) / 2>(tmem + t * 256 + lane_off + CF::PCOL + BK / 2, z);
           ptx::tmem_st_wait();
@@ -311,11 +315,13 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
           m4[(i >> 1) & 3] = ptx::fmax3(m4[(i >> 1) & 3], __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
         float pm = ptx::fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
         if (!slow) pm *= p.scale_log2;
-        // the two halves' partial maxima meet in shared memory (parity-buffered)
-        float* xj = xs + ((j & 1) * 4 + t * 2) * BQ;
-        xj[half * BQ + row] = pm;
-        ptx::named_bar_sync(bar_id, 64);
-        const float mx = fmaxf(pm, xj[(half ^ 1) * BQ + row]);
+        float mx = pm;
+        if constexpr (!FR) {  // the two halves' partial maxima meet in shared memory (parity-buffered)
+          float* xj = xs + ((j & 1) * 4 + t * 2) * BQ;
+          xj[half * BQ + row] = pm;
+          ptx::named_bar_sync(bar_id, 64);
+          mx = fmaxf(pm, xj[(half ^ 1) * BQ + row]);
+        }
         VC_TRP(trs, 2 + sw, j, 1);
         float alpha = 1.f;
         if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
@@ -352,7 +358,8 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
         VC_TRP(trs, 2 + sw, j, 3);
         ptx::tmem_st_cols<0, HK / 2>(tP, pk);  // 16 / 8 / 4-column pieces (x4 only: 2% slower)
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          if (half == 0) rescale_o<DP, 0, CF::NC0, CF::ON>(tO, alpha);
+          if (FR) rescale_o<DP, 0, CF::NC, CF::ON>(tO, alpha);
+          else if (half == 0) rescale_o<DP, 0, CF::NC0, CF::ON>(tO, alpha);
           else rescale_o<DP, CF::NC0, CF::NC, CF::ON>(tO, alpha);
         }
         ptx::tmem_st_wait();
@@ -368,13 +375,14 @@ __global__ void __launch_bounds__(kThreadsTp, 1)
         ptx::tmem_ld1(tO + p.dh, r1);
         ptx::tmem_ld_wait();
         l = __uint_as_float(r1);
-      } else {  // the two halves' partial sums (same alpha history) add up
+      } else if (!FR) {  // the two halves' partial sums (same alpha history) add up
         float* xj = xs + ((n_tiles & 1) * 4 + t * 2) * BQ;
         xj[half * BQ + row] = l;
         ptx::named_bar_sync(bar_id, 64);
         l += xj[(half ^ 1) * BQ + row];
       }
-      if (half == 0) store_out<DP, 0, CF::NC0, CF::ON>(p, tO, l, q0 + t * BQ + row, seq, h);
+      if (FR) store_out<DP, 0, CF::NC, CF::ON>(p, tO, l, q0 + t * BQ + row, seq, h);
+      else if (half == 0) store_out<DP, 0, CF::NC0, CF::ON>(p, tO, l, q0 + t * BQ + row, seq, h);
       else store_out<DP, CF::NC0, CF::NC, CF::ON>(p, tO, l, q0 + t * BQ + row, seq, h);
     }
   }
@@ -412,7 +420,7 @@ static int launch_attn_tp_narrow(const AttnTcParams& p, const void* q, const voi
     attr = true;
   }
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-  attn_tp_kernel<80, 4, true, true><<<grid, kThreadsTp, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);
+  attn_tp_kernel<80, 4, true, true><<<grid, CF::WARPS * 32, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
@@ -431,6 +439,29 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
   AttnMaps m;
   VC_TRY((make_attn_maps<DP, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
   static const int poly = tuning_int("VC_POLY_EVERY", 4);
+#ifdef VC_TUNING
+  static const int fr = tuning_int("VC_ATTN_FR", 0);
+  if (fr && poly == 4) {
+    using CFR = CfgTp<DP, false, true>;
+    static bool attr_fr = false;
+    if (!attr_fr) {
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, true, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CFR::SMEM));
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, false, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CFR::SMEM));
+      attr_fr = true;
+    }
+    dim3 grid_fr((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
+    if (ones)
+      attn_tp_kernel<DP, 4, true, false, true><<<grid_fr, CFR::WARPS * 32, CFR::SMEM, st>>>(m.q64, m.q16, m.k64,
+                                                                                            m.k16, m.v, p);
+    else
+      attn_tp_kernel<DP, 4, false, false, true><<<grid_fr, CFR::WARPS * 32, CFR::SMEM, st>>>(m.q64, m.q16, m.k64,
+                                                                                             m.k16, m.v, p);
+    VC_CHECK_LAUNCH();
+    return VC_OK;
+  }
+#endif
   dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
 #define VC_ATTN_TP_CASE(PV, ON)                                                                                  \
   if (poly == PV && ones == ON) {                                                                               \
@@ -440,7 +471,7 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
                                          CF::SMEM));                                                            \
       attr = true;                                                                                              \
     }                                                                                                           \
-    attn_tp_kernel<DP, PV, ON, false><<<grid, kThreadsTp, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);  \
+    attn_tp_kernel<DP, PV, ON, false><<<grid, CF::WARPS * 32, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);  \
     VC_CHECK_LAUNCH();                                                                                          \
     return VC_OK;                                                                                               \
   }

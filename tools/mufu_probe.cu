@@ -50,7 +50,47 @@ void run(const char* name, int per_op) {
   cudaFree(out);
 }
 
+// warp-level mma.sync m16n8k16 bf16 -> f32: 8 independent accumulators per warp
+__global__ void kmma(float* out) {
+  uint32_t a[4] = {threadIdx.x, threadIdx.x * 3u, threadIdx.x * 5u, threadIdx.x * 7u};
+  uint32_t b0 = threadIdx.x * 11u, b1 = threadIdx.x * 13u;
+  float d[8][4] = {};
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+          "{%0,%1,%2,%3};"
+          : "+f"(d[i][0]), "+f"(d[i][1]), "+f"(d[i][2]), "+f"(d[i][3])
+          : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+  float s = 0.f;
+  for (int i = 0; i < 8; ++i) s += d[i][0] + d[i][1] + d[i][2] + d[i][3];
+  if (s == 1.2345f) out[0] = s;
+}
+
 int main() {
+  {
+    float* out;
+    cudaMalloc(&out, 4);
+    int sms = 0, clk = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    for (int warps : {4, 8, 16, 32}) {
+      const int blocks = sms * 2, threads = warps * 16;
+      kmma<<<blocks, threads>>>(out);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0); cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      for (int r = 0; r < 5; ++r) kmma<<<blocks, threads>>>(out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      const double flop = 5.0 * blocks * (threads / 32) * (double)(ITERS / 4) * 8 * 2 * 16 * 8 * 16;
+      printf("mma.sync m16n8k16 bf16, %2d warps/SM: %.3f ms  %.1f TFLOP/s  (%.0f MAC/clk/SM at %d MHz)\n", warps, ms,
+             flop / (ms * 1e-3) / 1e12, flop / 2 / (ms * 1e-3) / (clk * 1e3) / sms, clk / 1000);
+    }
+  }
   run<0>("f32", 1);
   run<1>("f16x2", 2);
   run<2>("bf16x2", 2);
