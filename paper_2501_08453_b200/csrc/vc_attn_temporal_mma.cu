@@ -14,6 +14,7 @@
 // Out: o bf16 [rows][ldo] at head columns h*dh (pointer pre-offset)
 #include "vc_kernels.h"
 #include "vc_ptx.cuh"
+#include "vc_tuning.h"
 
 namespace vc {
 
@@ -43,26 +44,74 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool o
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
 
+// Long sequences (SHARED): one CTA per (position, head) stages the whole
+// sequence's K and V in shared memory ONCE (every warp of the CTA reads them;
+// per-warp staging re-reads them F/16 times and waits for each 16-key block),
+// then its warps take the 16-frame query tiles in turn (<= 8 warps, as many
+// as balance the tiles: 10 tiles -> 5 warps x 2).
+constexpr int kWarpsShared = 8;
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // KS: head-dim k-steps of 16 (dh <= 16*KS); NT: output n-tiles of 8 (dh <= 8*NT);
 // VEC16: the head slice of every row is 16-byte aligned (16-byte copies)
-template <int KS, int NT, bool VEC16>
-__global__ void __launch_bounds__(kWarps * 32)
+template <int KS, int NT, bool VEC16, bool SHARED>
+__global__ void __launch_bounds__(SHARED ? kWarpsShared * 32 : kWarps * 32, SHARED ? 2 : 1)
     temporal_mma_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int64_t D,
                         __nv_bfloat16* __restrict__ o, int64_t ldo, int F, int Lv, int H, int dh,
                         float scale_log2, int hs, int pos_major) {
   constexpr int KPAD = 16 * KS + 8;  // smem row pitch (elements): conflict-free ldmatrix
-  __shared__ __align__(16) __nv_bfloat16 sK[kWarps][16][KPAD];
-  __shared__ __align__(16) __nv_bfloat16 sV[kWarps][16][KPAD];
+  const int NW = SHARED ? (int)(blockDim.x >> 5) : kWarps;
+  __shared__ __align__(16) __nv_bfloat16 sKw[SHARED ? 1 : kWarps][16][KPAD];
+  __shared__ __align__(16) __nv_bfloat16 sVw[SHARED ? 1 : kWarps][16][KPAD];
+  extern __shared__ __align__(16) __nv_bfloat16 sKV[];  // SHARED: K [Fpad][KPAD], then V
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int QT = (F + 15) / 16;
-  const int64_t item = (int64_t)blockIdx.x * kWarps + warp;
-  if (item >= (int64_t)Lv * H * QT) return;
-  const int qt = (int)(item % QT);
-  const int h = (int)((item / QT) % H);
-  const int l = (int)(item / ((int64_t)QT * H));
-  const int f0 = qt * 16;
+  int qt0, h, l;
+  if constexpr (SHARED) {
+    h = (int)(blockIdx.x % (unsigned)H);  // heads fastest: concurrent CTAs read the same rows
+    l = (int)(blockIdx.x / (unsigned)H);
+    qt0 = warp;
+  } else {
+    const int64_t item = (int64_t)blockIdx.x * kWarps + warp;
+    if (item >= (int64_t)Lv * H * QT) return;
+    qt0 = (int)(item % QT);
+    h = (int)((item / QT) % H);
+    l = (int)(item / ((int64_t)QT * H));
+  }
   const int64_t col0 = (int64_t)h * dh;
+  const int words = 8 * KS;  // 32-bit words per padded row (16*KS bf16)
+  const int Fpad = QT * 16;
+  if constexpr (SHARED) {
+    // ---- the sequence's K and V rows (zero padded to Fpad x 16KS) into shared memory ----
+    __nv_bfloat16* sK = sKV;
+    __nv_bfloat16* sV = sKV + (size_t)Fpad * KPAD;
+    if (VEC16) {
+      constexpr int CH = 2 * KS;
+      for (int e = threadIdx.x; e < Fpad * CH; e += NW * 32) {
+        const int r = e / CH, c = (e - r * CH) * 8;
+        const bool ok = r < F && c < dh;
+        const int64_t rr0 = pos_major ? (int64_t)l * F + (ok ? r : 0) : (int64_t)(ok ? r : 0) * Lv + l;
+        const __nv_bfloat16* row = qkv + rr0 * ld + col0 + (ok ? c : 0);
+        cp_async16(ptx::smem_u32(sK + r * KPAD + c), row + D, ok);
+        cp_async16(ptx::smem_u32(sV + r * KPAD + c), row + 2 * D, ok);
+      }
+    } else {
+      for (int e = threadIdx.x; e < Fpad * words; e += NW * 32) {
+        const int r = e / words, c = 2 * (e - r * words);
+        const bool ok = r < F && c < dh;
+        const int64_t rr0 = pos_major ? (int64_t)l * F + (ok ? r : 0) : (int64_t)(ok ? r : 0) * Lv + l;
+        const __nv_bfloat16* row = qkv + rr0 * ld + col0 + (ok ? c : 0);
+        cp_async4(ptx::smem_u32(sK + r * KPAD + c), row + D, ok);
+        cp_async4(ptx::smem_u32(sV + r * KPAD + c), row + 2 * D, ok);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  for (int qt = qt0; qt < QT; qt += SHARED ? NW : QT) {
+  const int f0 = qt * 16;
 
   // ---- Q fragments (A operand, row-major 16 x 16 per k-step), zero padded ----
   uint32_t qa[KS][4];
@@ -84,10 +133,13 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
   for (int j = 0; j < NT; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  const uint32_t kbase = ptx::smem_u32(&sK[warp][0][0]), vbase = ptx::smem_u32(&sV[warp][0][0]);
-  const int words = 8 * KS;  // 32-bit words per padded row (16*KS bf16)
+  uint32_t kbase = SHARED ? ptx::smem_u32(sKV) : ptx::smem_u32(&sKw[SHARED ? 0 : warp][0][0]);
+  uint32_t vbase = SHARED ? ptx::smem_u32(sKV + (size_t)Fpad * KPAD) : ptx::smem_u32(&sVw[SHARED ? 0 : warp][0][0]);
 
   for (int k0 = 0; k0 < F; k0 += 16) {
+    if constexpr (SHARED) {
+      if (k0 > 0) { kbase += 16 * KPAD * 2; vbase += 16 * KPAD * 2; }
+    } else {
     // ---- stage K and V rows of this 16-key block (zero padded) with async
     //      copies: all loads in flight at once, no register round trip ----
     __syncwarp();
@@ -99,8 +151,8 @@ __global__ void __launch_bounds__(kWarps * 32)
         const bool ok = fr < F && c < dh;
         const int64_t rr0 = pos_major ? (int64_t)l * F + (ok ? fr : 0) : (int64_t)(ok ? fr : 0) * Lv + l;
         const __nv_bfloat16* row = qkv + rr0 * ld + col0 + (ok ? c : 0);
-        cp_async16(ptx::smem_u32(&sK[warp][r][c]), row + D, ok);
-        cp_async16(ptx::smem_u32(&sV[warp][r][c]), row + 2 * D, ok);
+        cp_async16(ptx::smem_u32(&sKw[SHARED ? 0 : warp][r][c]), row + D, ok);
+        cp_async16(ptx::smem_u32(&sVw[SHARED ? 0 : warp][r][c]), row + 2 * D, ok);
       }
     } else {
       for (int e = lane; e < 16 * words; e += 32) {
@@ -109,12 +161,13 @@ __global__ void __launch_bounds__(kWarps * 32)
         const bool ok = fr < F && c < dh;
         const int64_t rr0 = pos_major ? (int64_t)l * F + (ok ? fr : 0) : (int64_t)(ok ? fr : 0) * Lv + l;
         const __nv_bfloat16* row = qkv + rr0 * ld + col0 + (ok ? c : 0);
-        cp_async4(ptx::smem_u32(&sK[warp][r][c]), row + D, ok);
-        cp_async4(ptx::smem_u32(&sV[warp][r][c]), row + 2 * D, ok);
+        cp_async4(ptx::smem_u32(&sKw[SHARED ? 0 : warp][r][c]), row + D, ok);
+        cp_async4(ptx::smem_u32(&sVw[SHARED ? 0 : warp][r][c]), row + 2 * D, ok);
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
+    }
 
     // ---- S = Q K^T for keys k0..k0+15 (two n-tiles of 8 keys) ----
     float s[2][4];
@@ -239,20 +292,40 @@ __global__ void __launch_bounds__(kWarps * 32)
       if (fr1 < F) *reinterpret_cast<__nv_bfloat162*>(o1 + c) = __floats2bfloat162_rn(oacc[j][2] * i1, oacc[j][3] * i1);
     }
   }
+  }  // query tiles
 }
 
 template <int KS, int NT>
 int launch_ks(const __nv_bfloat16* qkv, int64_t ld, int64_t D, __nv_bfloat16* o, int64_t ldo, int F, int Lv,
               int H, int dh, cudaStream_t st, int hs, int pm) {
+  const float sl2 = (float)(1.4426950408889634 / sqrt((double)dh));
+  const bool vec16 = dh % 8 == 0 && ld % 8 == 0 && D % 8 == 0 && ((uintptr_t)qkv % 16) == 0;
+  // long sequences: K / V staged once per (position, head) CTA (measured rule, profiles/r02/temporal)
+  static const int min_shared = tuning_int("VC_TEMPORAL_SHARED_MIN_F", 48);
+  const int Fpad = (F + 15) / 16 * 16;
+  const size_t smem = (size_t)2 * Fpad * (16 * KS + 8) * 2;
+  if (F >= min_shared && smem <= 110 * 1024) {
+    const int64_t blocks = (int64_t)Lv * H;
+    if (blocks > 2147483647) { set_error("temporal grid too large"); return VC_ENOTSUP; }
+    auto kern = vec16 ? temporal_mma_kernel<KS, NT, true, true> : temporal_mma_kernel<KS, NT, false, true>;
+    static bool attr[2] = {false, false};
+    if (!attr[vec16]) {
+      VC_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+      attr[vec16] = true;
+    }
+    const int QT = Fpad / 16, rounds = (QT + kWarpsShared - 1) / kWarpsShared;
+    const int nw = (QT + rounds - 1) / rounds;  // warps that balance the query tiles
+    kern<<<(unsigned)blocks, nw * 32, smem, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs, pm);
+    VC_CHECK_LAUNCH();
+    return VC_OK;
+  }
   const int64_t items = (int64_t)Lv * H * ((F + 15) / 16);
   const int64_t blocks = cdiv(items, kWarps);
   if (blocks > 2147483647) { set_error("temporal grid too large"); return VC_ENOTSUP; }
-  const float sl2 = (float)(1.4426950408889634 / sqrt((double)dh));
-  const bool vec16 = dh % 8 == 0 && ld % 8 == 0 && D % 8 == 0 && ((uintptr_t)qkv % 16) == 0;
   if (vec16)
-    temporal_mma_kernel<KS, NT, true><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs, pm);
+    temporal_mma_kernel<KS, NT, true, false><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs, pm);
   else
-    temporal_mma_kernel<KS, NT, false><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs, pm);
+    temporal_mma_kernel<KS, NT, false, false><<<(unsigned)blocks, kWarps * 32, 0, st>>>(qkv, ld, D, o, ldo, F, Lv, H, dh, sl2, hs, pm);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
