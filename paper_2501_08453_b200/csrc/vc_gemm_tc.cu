@@ -366,11 +366,12 @@ __device__ __forceinline__ void qkvn_head(const GemmTcParams& p, int64_t m, int 
 // (M) sweeping all N tiles, so the ~148 tiles in flight touch only a few A
 // row-panels and B column-panels and both stay resident in L2.
 constexpr int kGroupM = 4;
-__device__ __forceinline__ void tile_coords(int ct, int num_mc, int num_n, int& mc, int& nt) {
-  const int per_group = kGroupM * num_n;
+__device__ __forceinline__ void tile_coords(int ct, int num_mc, int num_n, int& mc, int& nt, int group_m = 0) {
+  const int gm = group_m > 0 ? group_m : kGroupM;
+  const int per_group = gm * num_n;
   const int g = ct / per_group, r = ct - g * per_group;
-  const int first = g * kGroupM;
-  const int gsize = min(num_mc - first, kGroupM);
+  const int first = g * gm;
+  const int gsize = min(num_mc - first, gm);
   mc = first + r % gsize;
   nt = r / gsize;
 }
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0; uint32_t ph = 0;
       for (int ct = cluster; ct < ctiles; ct += nclusters) {
         int mc, nt;
-        tile_coords(ct, num_mc, num_n, mc, nt);
+        tile_coords(ct, num_mc, num_n, mc, nt, p.group_m);
         const int mt = mc * CM + rank;
         for (int kb = 0; kb < kblocks; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int ct = cluster; ct < ctiles; ct += nclusters, ++local) {
       const int acc = local & 1;
       int mc, nt;
-        tile_coords(ct, num_mc, num_n, mc, nt);
+        tile_coords(ct, num_mc, num_n, mc, nt, p.group_m);
         const int mt = mc * CM + rank;
       // this tile's bias columns -> a per-warp smem copy (read back as broadcasts)
       if (p.bias) {
@@ -599,7 +600,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       int s = 0; uint32_t ph = 0;
       for (int t = cluster; t < tiles; t += nclusters) {
         int mt, ntc;
-        tile_coords(t, num_m, num_nc, mt, ntc);
+        tile_coords(t, num_m, num_nc, mt, ntc, p.group_m);
         const int nt = ntc * NP + pair;  // may be >= num_n (odd count): B is OOB, no output
         for (int kb = 0; kb < kblocks; ++kb) {
           ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     for (int t = cluster; t < tiles; t += nclusters, ++local) {
       const int acc = local & 1;
       int mt, ntc;
-      tile_coords(t, num_m, num_nc, mt, ntc);
+      tile_coords(t, num_m, num_nc, mt, ntc, p.group_m);
       const int nt = ntc * NP + pair;
       if (p.bias) {
         __syncwarp();
@@ -935,9 +936,15 @@ static int launch_gemm_tc_ext(const void* A, int64_t lda, const void* B, int64_t
   return VC_ENOTSUP;
 }
 
-int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const GemmTcParams& p,
+int launch_gemm_tc(const void* A, int64_t lda, const void* B, int64_t ldb, const GemmTcParams& p_in,
                    int epi, cudaStream_t st, int bn) {
-  if (p.M <= 0 || p.N <= 0) return VC_OK;
+  if (p_in.M <= 0 || p_in.N <= 0) return VC_OK;
+  GemmTcParams p = p_in;
+  // M tiles per rasterization group: 32 for the QKV GEMM (N = 9D wide: fewer
+  // re-reads of the weight panels, 0.771 vs 0.816 ms at kGroupM = 4), the
+  // default 4 elsewhere (the O GEMM: 0.251 vs 0.292 at 32); tools/ab_bench.sh
+  static const int group_env = tuning_int("VC_GEMM_GROUPM", 0);
+  if (!p.group_m) p.group_m = group_env ? group_env : (epi == EPI_QKV ? 32 : 0);
   if (epi >= EPI_QKVN) {
     if (p.K <= 0 || (lda * 2) % 16 || (ldb * 2) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) {
       set_error("tcgen05 GEMM needs 16-byte aligned operands and row pitches");

@@ -75,6 +75,7 @@ struct GemmTcParams {
   int64_t ldo;
   const float* gate;  // EPI_F32G: [N]
   QkvScatter qkv;
+  int32_t group_m;    // M tiles per rasterization group (0: the default, kGroupM)
 };
 
 // C = A[M][K] . B[N][K]^T with the selected epilogue.  A/B bf16 K-major.
