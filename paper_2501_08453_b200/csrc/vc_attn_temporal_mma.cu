@@ -56,7 +56,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // KS: head-dim k-steps of 16 (dh <= 16*KS); NT: output n-tiles of 8 (dh <= 8*NT);
 // VEC16: the head slice of every row is 16-byte aligned (16-byte copies)
 template <int KS, int NT, bool VEC16, bool SHARED>
-__global__ void __launch_bounds__(SHARED ? kWarpsShared * 32 : kWarps * 32, SHARED ? 2 : 1)
+__global__ void __launch_bounds__(SHARED ? kWarpsShared * 32 : kWarps * 32, SHARED ? 2 : KS <= 6 ? 4 : 1)
     temporal_mma_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, int64_t D,
                         __nv_bfloat16* __restrict__ o, int64_t ldo, int F, int Lv, int H, int dh,
                         float scale_log2, int hs, int pos_major) {
@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(SHARED ? kWarpsShared * 32 : kWarps * 32, SHAR
     cp_async_wait_all();
     __syncthreads();
   }
-  for (int qt = qt0; qt < QT; qt += SHARED ? NW : QT) {
+  // one 16-frame query tile (a lambda so the per-warp kernel keeps its
+  // straight-line register allocation: no loop-carried state)
+  auto attend_tile = [&](const int qt) {
   const int f0 = qt * 16;
 
   // ---- Q fragments (A operand, row-major 16 x 16 per k-step), zero padded ----
@@ -292,7 +294,12 @@ __global__ void __launch_bounds__(SHARED ? kWarpsShared * 32 : kWarps * 32, SHAR
       if (fr1 < F) *reinterpret_cast<__nv_bfloat162*>(o1 + c) = __floats2bfloat162_rn(oacc[j][2] * i1, oacc[j][3] * i1);
     }
   }
-  }  // query tiles
+  };
+  if constexpr (SHARED) {
+    for (int qt = qt0; qt < QT; qt += NW) attend_tile(qt);
+  } else {
+    attend_tile(qt0);
+  }
 }
 
 template <int KS, int NT>

@@ -78,7 +78,10 @@ __device__ unsigned long long g_attn_cta[16384][5];
 // FR (full row): one softmax thread per query row (4 warps per tile, 12
 // warps: w0 TMA, w1 / w2 MMA issuers, w3 idle, w4..w11 softmax) instead of
 // two warps per row meeting in shared memory for the row max.
-template <int DP, bool NARROW = false, bool FR = false>
+// NT: query tiles per CTA. NT = 1 (short sequences: the spatial branch):
+// 256 TMEM columns and a 2-deep K / V ring, so two CTAs share an SM and one's
+// prologue / epilogue runs under the other's main loop.
+template <int DP, bool NARROW = false, bool FR = false, int NT = 2>
 struct CfgTp {
   static constexpr int N64 = DP / 64;
   static constexpr int TAIL = DP % 64;
@@ -87,7 +90,8 @@ struct CfgTp {
   static_assert(!NARROW || DP == 80, "the narrow layout is the DP 80 one");
   static constexpr int BK = NARROW ? 120 : DP == 64 ? 128 : 112;  // keys per block
   static constexpr int HK = FR ? BK : BK / 2;                     // keys per softmax thread
-  static constexpr int WARPS = FR ? 12 : 19;
+  static constexpr int WARPS = FR ? 4 + 4 * NT : 3 + 8 * NT;
+  static constexpr int TMEM_COLS = 256 * NT;
   static constexpr int SM0 = FR ? 4 : 3;                          // first softmax warp
   static constexpr int SM_ARRIVALS = FR ? 128 : 256;              // softmax threads per tile
   static constexpr int PKEYS = NARROW ? 128 : BK;                 // the P.V K extent
@@ -98,9 +102,9 @@ struct CfgTp {
   static constexpr int K_BYTES = BK * DP * 2;
   static constexpr int K_STAGE = (K_BYTES + 1023) / 1024 * 1024;  // SW128 tiles start 1024-aligned
   static constexpr int V_BYTES = DP * 128 * 2;  // two 64-key TMA boxes (keys past BK unused)
-  static constexpr int KS = 3;
+  static constexpr int KS = NT == 1 ? 2 : 3;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+  static constexpr int OFF_K = OFF_Q + NT * Q_BYTES;
   static constexpr int OFF_V = OFF_K + KS * K_STAGE;
   static constexpr int OFF_X = OFF_V + KS * V_BYTES;       // row-max exchange [2][2 tiles][2 halves][128]
   static constexpr int OFF_BAR = OFF_X + 2 * 2 * 2 * BQ * 4;
@@ -111,12 +115,12 @@ struct CfgTp {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, int POLY, bool ONES, bool NARROW, bool FR = false>
-__global__ void __launch_bounds__(CfgTp<DP, NARROW, FR>::WARPS * 32, 1)
+template <int DP, int POLY, bool ONES, bool NARROW, bool FR = false, int NT = 2>
+__global__ void __launch_bounds__(CfgTp<DP, NARROW, FR, NT>::WARPS * 32, NT == 1 ? 2 : 1)
     attn_tp_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
                    const __grid_constant__ CUtensorMap tmV, const AttnTcParams p) {
-  using CF = CfgTp<DP, NARROW, FR>;
+  using CF = CfgTp<DP, NARROW, FR, NT>;
   constexpr int KS = CF::KS, BK = CF::BK, HK = CF::HK;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -133,11 +137,11 @@ __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR>::WARPS * 32, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5;
-  const int q0 = blockIdx.x * (2 * BQ);
+  const int q0 = blockIdx.x * (NT * BQ);
   const int h = blockIdx.y;
   const int seq = blockIdx.z;
   const int n_tiles = (p.Lk + BK - 1) / BK;
-  const int ntile = q0 + BQ < p.Lq ? 2 : 1;  // the last CTA of a sequence may hold one tile
+  const int ntile = NT == 1 ? 1 : q0 + BQ < p.Lq ? 2 : 1;  // the last CTA of a sequence may hold one tile
   [[maybe_unused]] const bool tr = blockIdx.x == min(20u, gridDim.x - 1) && blockIdx.y == 3 && blockIdx.z == 0;
   if (threadIdx.x == 0) VC_CTA(0);
 
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR>::WARPS * 32, 1)
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, CF::TMEM_COLS);
   ptx::fence_before_sync();
   __syncthreads();
   ptx::fence_after_sync();
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR>::WARPS * 32, 1)
   if (threadIdx.x == 0) VC_CTA(3);
   if (warp == 1) {
     ptx::fence_after_sync();
-    ptx::tmem_dealloc(tmem, 512);
+    ptx::tmem_dealloc(tmem, CF::TMEM_COLS);
   }
 }
 
@@ -439,6 +443,30 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
   AttnMaps m;
   VC_TRY((make_attn_maps<DP, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
   static const int poly = tuning_int("VC_POLY_EVERY", 4);
+  // one query tile per CTA, two CTAs per SM for short key ranges (the spatial
+  // branch: 0.318 vs 0.328 ms at config 2, tools/ab_bench.sh; 3.86 vs 3.39 ms
+  // on the full sequence, where K / V traffic doubles). VC_ATTN_1T: 0 off, 2 always.
+  static const int one_tile = tuning_int("VC_ATTN_1T", 1);
+  if (one_tile && poly == 4 && (one_tile == 2 || p.Lk <= 4096)) {
+    using C1 = CfgTp<DP, false, false, 1>;
+    static bool attr_1t = false;
+    if (!attr_1t) {
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, true, false, false, 1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
+      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, false, false, false, 1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
+      attr_1t = true;
+    }
+    dim3 grid_1t((unsigned)cdiv(p.Lq, BQ), (unsigned)p.H, (unsigned)nseq);
+    if (ones)
+      attn_tp_kernel<DP, 4, true, false, false, 1><<<grid_1t, C1::WARPS * 32, C1::SMEM, st>>>(m.q64, m.q16, m.k64,
+                                                                                              m.k16, m.v, p);
+    else
+      attn_tp_kernel<DP, 4, false, false, false, 1><<<grid_1t, C1::WARPS * 32, C1::SMEM, st>>>(m.q64, m.q16, m.k64,
+                                                                                               m.k16, m.v, p);
+    VC_CHECK_LAUNCH();
+    return VC_OK;
+  }
 #ifdef VC_TUNING
   static const int fr = tuning_int("VC_ATTN_FR", 0);
   if (fr && poly == 4) {
