@@ -14,6 +14,14 @@ namespace attn {
 
 constexpr int BQ = 128, BKV = 128;
 constexpr float kRescaleThreshold = 8.0f;
+// Fixed-offset softmax (attn_tp_kernel FIXM): the row's exponent offset is
+// set once, from the exact max of the first key block, to max + this margin
+// (log2 units), and never moves: P = 2^(x - m) <= 1 for every key within the
+// margin of that max, P <= 2^127 (no overflow) for any key up to 187 above
+// it, and the first block's max element keeps P = 2^-60 (far from fp32 / bf16
+// subnormals). softmax is shift-invariant, so O / l is unchanged; no per-block
+// row max, exchange or rescale.
+constexpr float kFixedMaxMargin = 60.0f;
 
 // smem descriptor of head-dim 16-chunk c of a [128 rows][DP] Q/K tile laid out
 // as N64 SW128 sub-tiles [128][128 B] followed by the SW32 tail [128][32 B]

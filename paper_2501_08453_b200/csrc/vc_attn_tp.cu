@@ -115,7 +115,7 @@ struct CfgTp {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, int POLY, bool ONES, bool NARROW, bool FR = false, int NT = 2>
+template <int DP, int POLY, bool ONES, bool NARROW, bool FR = false, int NT = 2, bool FIXM = false>
 __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR, NT>::WARPS * 32, NT == 1 ? 2 : 1)
     attn_tp_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
@@ -312,26 +312,30 @@ __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR, NT>::WARPS * 32, NT == 1
             r[i] = __float_as_uint(x);
           }
         }
-        // row max of this half: four FMNMX3 chains (two logits per instruction)
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        float alpha = 1.f;
+        if (!FIXM || j == 0) {
+          // row max of this half: four FMNMX3 chains (two logits per instruction)
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int i = 0; i < HK; i += 2)
-          m4[(i >> 1) & 3] = ptx::fmax3(m4[(i >> 1) & 3], __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
-        float pm = ptx::fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
-        if (!slow) pm *= p.scale_log2;
-        float mx = pm;
-        if constexpr (!FR) {  // the two halves' partial maxima meet in shared memory (parity-buffered)
-          float* xj = xs + ((j & 1) * 4 + t * 2) * BQ;
-          xj[half * BQ + row] = pm;
-          ptx::named_bar_sync(bar_id, 64);
-          mx = fmaxf(pm, xj[(half ^ 1) * BQ + row]);
+          for (int i = 0; i < HK; i += 2)
+            m4[(i >> 1) & 3] = ptx::fmax3(m4[(i >> 1) & 3], __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+          float pm = ptx::fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+          if (!slow) pm *= p.scale_log2;
+          float mx = pm;
+          if constexpr (!FR) {  // the two halves' partial maxima meet in shared memory (parity-buffered)
+            float* xj = xs + ((j & 1) * 4 + t * 2) * BQ;
+            xj[half * BQ + row] = pm;
+            ptx::named_bar_sync(bar_id, 64);
+            mx = fmaxf(pm, xj[(half ^ 1) * BQ + row]);
+          }
+          if (FIXM) {
+            m_used = mx + kFixedMaxMargin;  // fixed for the whole row from here on
+          } else if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
+            alpha = ptx::ex2(m_used - mx);                // 0 on the first block
+            m_used = mx;
+          }
         }
         VC_TRP(trs, 2 + sw, j, 1);
-        float alpha = 1.f;
-        if (mx > m_used + kRescaleThreshold) {  // lazy rescale: P stays <= 2^8
-          alpha = ptx::ex2(m_used - mx);         // 0 on the first block
-          m_used = mx;
-        }
         const float sc = slow ? 1.f : p.scale_log2;
         const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m_used, -m_used);
         float2 s2 = make_float2(0.f, 0.f), s2b = make_float2(0.f, 0.f);
@@ -410,111 +414,65 @@ int attn_cta_read(unsigned long long* host) {  // [16384][5]
 }
 #endif
 
-#ifdef VC_TUNING
-// measured-and-dropped variant (profiles/r02/attn/README.md): tuning builds only
-static int launch_attn_tp_narrow(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
-                                 int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
-  using CF = CfgTp<80, true>;
+// One launch of a kernel variant (maps built with its key-block rows).
+template <int DP, int POLY, bool ONES, bool NARROW, bool FR, int NT, bool FIXM>
+int run_tp(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq, int64_t q_rows_per_seq,
+           int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
+  using CF = CfgTp<DP, NARROW, FR, NT>;
   AttnMaps m;
-  VC_TRY((make_attn_maps<80, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
+  VC_TRY((make_attn_maps<DP, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
+  auto kern = attn_tp_kernel<DP, POLY, ONES, NARROW, FR, NT, FIXM>;
   static bool attr = false;
   if (!attr) {
-    VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<80, 4, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       CF::SMEM));
+    VC_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr = true;
   }
-  dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-  attn_tp_kernel<80, 4, true, true><<<grid, CF::WARPS * 32, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);
+  dim3 grid((unsigned)cdiv(p.Lq, NT * BQ), (unsigned)p.H, (unsigned)nseq);
+  kern<<<grid, CF::WARPS * 32, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }
-#endif
 
 template <int DP>
 int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq,
                    int64_t q_rows_per_seq, int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
   const bool ones = p.dh < DP;
-#ifdef VC_TUNING
-  static const int narrow_on = tuning_int("VC_ATTN_NARROW", 0);
-  if (DP == 80 && ones && p.dh < 72 && narrow_on) return launch_attn_tp_narrow(p, q, k, vt, nseq, q_rows_per_seq,
-                                                                           k_rows_per_seq, ld_key, st);
-#endif
-  using CF = CfgTp<DP>;
-  AttnMaps m;
-  VC_TRY((make_attn_maps<DP, CF::BK>(m, p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key)));
-  static const int poly = tuning_int("VC_POLY_EVERY", 4);
+#define VC_TP_ARGS p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st
   // one query tile per CTA, two CTAs per SM for short key ranges (the spatial
   // branch: 0.318 vs 0.328 ms at config 2, tools/ab_bench.sh; 3.86 vs 3.39 ms
   // on the full sequence, where K / V traffic doubles). VC_ATTN_1T: 0 off, 2 always.
   static const int one_tile = tuning_int("VC_ATTN_1T", 1);
-  if (one_tile && poly == 4 && (one_tile == 2 || p.Lk <= 4096)) {
-    using C1 = CfgTp<DP, false, false, 1>;
-    static bool attr_1t = false;
-    if (!attr_1t) {
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, true, false, false, 1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, false, false, false, 1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
-      attr_1t = true;
-    }
-    dim3 grid_1t((unsigned)cdiv(p.Lq, BQ), (unsigned)p.H, (unsigned)nseq);
-    if (ones)
-      attn_tp_kernel<DP, 4, true, false, false, 1><<<grid_1t, C1::WARPS * 32, C1::SMEM, st>>>(m.q64, m.q16, m.k64,
-                                                                                              m.k16, m.v, p);
-    else
-      attn_tp_kernel<DP, 4, false, false, false, 1><<<grid_1t, C1::WARPS * 32, C1::SMEM, st>>>(m.q64, m.q16, m.k64,
-                                                                                               m.k16, m.v, p);
-    VC_CHECK_LAUNCH();
-    return VC_OK;
-  }
+  const bool nt1 = one_tile == 2 || (one_tile == 1 && p.Lk <= 4096);
+  // fixed-offset softmax (kFixedMaxMargin: no per-block row max, half-row
+  // exchange or rescale after the first key block): full sequence 3.13 ->
+  // 2.84 ms, spatial 0.320 -> 0.287 ms at config 2 (tools/ab_bench.sh, 3
+  // rounds). VC_ATTN_FIXM=0: the lazy-rescale online softmax.
+  static const int fixm = tuning_int("VC_ATTN_FIXM", 1);
 #ifdef VC_TUNING
+  // measured-and-dropped variants (profiles/r02/attn/README.md): tuning builds only
+  static const int poly = tuning_int("VC_POLY_EVERY", 4);
+  static const int narrow_on = tuning_int("VC_ATTN_NARROW", 0);
   static const int fr = tuning_int("VC_ATTN_FR", 0);
-  if (fr && poly == 4) {
-    using CFR = CfgTp<DP, false, true>;
-    static bool attr_fr = false;
-    if (!attr_fr) {
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, true, false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CFR::SMEM));
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, 4, false, false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CFR::SMEM));
-      attr_fr = true;
-    }
-    dim3 grid_fr((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-    if (ones)
-      attn_tp_kernel<DP, 4, true, false, true><<<grid_fr, CFR::WARPS * 32, CFR::SMEM, st>>>(m.q64, m.q16, m.k64,
-                                                                                            m.k16, m.v, p);
-    else
-      attn_tp_kernel<DP, 4, false, false, true><<<grid_fr, CFR::WARPS * 32, CFR::SMEM, st>>>(m.q64, m.q16, m.k64,
-                                                                                             m.k16, m.v, p);
-    VC_CHECK_LAUNCH();
-    return VC_OK;
+  if (DP == 80 && ones && p.dh < 72 && narrow_on) return run_tp<80, 4, true, true, false, 2, false>(VC_TP_ARGS);
+  if (fr) return ones ? run_tp<DP, 4, true, false, true, 2, false>(VC_TP_ARGS)
+                      : run_tp<DP, 4, false, false, true, 2, false>(VC_TP_ARGS);
+  if (poly != 4 && ones) {
+    if (poly == 0) return run_tp<DP, 0, true, false, false, 2, false>(VC_TP_ARGS);
+    if (poly == 2) return run_tp<DP, 2, true, false, false, 2, false>(VC_TP_ARGS);
+    if (poly == 3) return run_tp<DP, 3, true, false, false, 2, false>(VC_TP_ARGS);
+    if (poly == 6) return run_tp<DP, 6, true, false, false, 2, false>(VC_TP_ARGS);
+    if (poly == 8) return run_tp<DP, 8, true, false, false, 2, false>(VC_TP_ARGS);
   }
 #endif
-  dim3 grid((unsigned)cdiv(p.Lq, 2 * BQ), (unsigned)p.H, (unsigned)nseq);
-#define VC_ATTN_TP_CASE(PV, ON)                                                                                  \
-  if (poly == PV && ones == ON) {                                                                               \
-    static bool attr = false;                                                                                   \
-    if (!attr) {                                                                                                \
-      VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tp_kernel<DP, PV, ON, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         CF::SMEM));                                                            \
-      attr = true;                                                                                              \
-    }                                                                                                           \
-    attn_tp_kernel<DP, PV, ON, false><<<grid, CF::WARPS * 32, CF::SMEM, st>>>(m.q64, m.q16, m.k64, m.k16, m.v, p);  \
-    VC_CHECK_LAUNCH();                                                                                          \
-    return VC_OK;                                                                                               \
-  }
-  VC_ATTN_TP_CASE(4, true)
-  VC_ATTN_TP_CASE(4, false)
-#ifdef VC_TUNING
-  VC_ATTN_TP_CASE(2, true)
-  VC_ATTN_TP_CASE(3, true)
-  VC_ATTN_TP_CASE(6, true)
-  VC_ATTN_TP_CASE(8, true)
-  VC_ATTN_TP_CASE(0, true)
-#endif
-#undef VC_ATTN_TP_CASE
-  set_error("attention variant not built (tuning builds: VC_POLY_EVERY 0, 2, 3, 4)");
-  return VC_EINVAL;
+#define VC_TP_PICK(ON)                                                                                   \
+  if (nt1) return fixm ? run_tp<DP, 4, ON, false, false, 1, true>(VC_TP_ARGS)                           \
+                       : run_tp<DP, 4, ON, false, false, 1, false>(VC_TP_ARGS);                         \
+  return fixm ? run_tp<DP, 4, ON, false, false, 2, true>(VC_TP_ARGS)                                    \
+              : run_tp<DP, 4, ON, false, false, 2, false>(VC_TP_ARGS);
+  if (ones) { VC_TP_PICK(true) }
+  VC_TP_PICK(false)
+#undef VC_TP_PICK
+#undef VC_TP_ARGS
 }
 
 template int launch_attn_tp<64>(const AttnTcParams&, const void*, const void*, const void*, int, int64_t, int64_t,

@@ -135,3 +135,29 @@ def test_persistent_variant_matches_oracle(vc):
     env = dict(os.environ, VC_ATTN_PERSIST="2", PYTHONPATH=root)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("sk", [600, 5000])  # one-tile (short) and two-tile CTAs
+def test_bf16_attention_logit_range_across_key_blocks(vc, sk):
+    # The softmax offset is fixed from the first key block's exact max (+60 in
+    # log2 units, vc_attn_tc_common.cuh kFixedMaxMargin): keys of later blocks
+    # whose logits lie ~140 log2 units ABOVE every first-block logit must still
+    # give the exact softmax (no overflow, no lost mass). Inputs are bf16-exact
+    # (20 x multiples of 1/64), so the logits themselves carry no rounding.
+    sq, dh = 200, 66
+    r = np.random.default_rng(11)
+    q = np.zeros((sq, dh)); q[:, 0] = 20.0
+    k = np.zeros((sk, dh))
+    k[:112, 0] = -20.0                                           # first block: logits -49 nats
+    k[112:, 0] = 20.0 * r.choice([0.90625, 0.9375, 0.96875, 1.0], sk - 112)  # later: +44..+49 nats
+    v = r.standard_normal((sk, dh))
+    got = vc.attention(q, k, v, 1, dtype="bf16")
+    ref = O.attention(q, k, v, 1)
+    assert np.isfinite(got).all()
+    assert rel_l2(got, ref) <= BF16_TOL, rel_l2(got, ref)
+    # and the mirror image: the first block holds the largest logits by far
+    k2 = -k
+    got2 = vc.attention(q, k2, v, 1, dtype="bf16")
+    ref2 = O.attention(q, k2, v, 1)
+    assert np.isfinite(got2).all()
+    assert rel_l2(got2, ref2) <= BF16_TOL, rel_l2(got2, ref2)
