@@ -53,7 +53,7 @@ struct Cfg {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP>
+template <int DP, bool FIXM>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
@@ -211,20 +211,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         scale = 1.f;
       }
-      float mx;
-      {
+      float alpha = 1.f;
+      if (!FIXM || j == 0) {  // FIXM: the offset is fixed after the first tile (kFixedMaxMargin)
         float m8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) m8[i] = v[i];
 #pragma unroll
         for (int i = 8; i < BKV; ++i) m8[i & 7] = fmaxf(m8[i & 7], v[i]);
-        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale;
-      }
-      float alpha = 1.f;
-      if (mx > m_used + kRescaleThreshold) {
-        alpha = ptx::ex2(m_used - mx);  // 0 on the first tile
-        m_used = mx;
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale;
+        if (FIXM) {
+          m_used = mx + kFixedMaxMargin;
+        } else if (mx > m_used + kRescaleThreshold) {
+          alpha = ptx::ex2(m_used - mx);  // 0 on the first tile
+          m_used = mx;
+        }
       }
       // p = 2^(s*scale - m): FFMA2 (two logits per instruction) + MUFU.EX2;
       // row sum in four FADD2 partials
@@ -324,13 +325,17 @@ int launch_dp(const AttnTcParams& p, const void* q, const void* k, const void* v
     const uint32_t box[4] = {64, DP, 1, 1};
     VC_TRY(make_tmap_4d_bf16(&mv, vt, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B));
   }
-  static bool attr = false;
-  if (!attr) {
-    VC_CHECK_CUDA(cudaFuncSetAttribute(attn_tc_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
-    attr = true;
+  // fixed-offset softmax after the first key tile (vc_attn_tc_common.cuh
+  // kFixedMaxMargin); VC_ATTN_FIXM=0: lazy rescale
+  static const int fixm = tuning_int("VC_ATTN_FIXM", 1);
+  auto kern = fixm ? attn_tc_kernel<DP, true> : attn_tc_kernel<DP, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[fixm ? 1 : 0]) {
+    VC_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    attr[fixm ? 1 : 0] = true;
   }
   dim3 grid((unsigned)cdiv(p.Lq, BQ), (unsigned)p.H, (unsigned)nseq);
-  attn_tc_kernel<DP><<<grid, kThreads, CF::SMEM, st>>>(mq64, mq16, mk64, mk16, mv, p);
+  kern<<<grid, kThreads, CF::SMEM, st>>>(mq64, mq16, mk64, mk16, mv, p);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }

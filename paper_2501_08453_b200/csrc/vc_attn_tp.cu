@@ -453,15 +453,15 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
   static const int poly = tuning_int("VC_POLY_EVERY", 4);
   static const int narrow_on = tuning_int("VC_ATTN_NARROW", 0);
   static const int fr = tuning_int("VC_ATTN_FR", 0);
-  if (DP == 80 && ones && p.dh < 72 && narrow_on) return run_tp<80, 4, true, true, false, 2, false>(VC_TP_ARGS);
+  if (DP == 80 && ones && p.dh < 72 && narrow_on) return run_tp<80, 4, true, true, false, 2, true>(VC_TP_ARGS);
   if (fr) return ones ? run_tp<DP, 4, true, false, true, 2, false>(VC_TP_ARGS)
                       : run_tp<DP, 4, false, false, true, 2, false>(VC_TP_ARGS);
   if (poly != 4 && ones) {
-    if (poly == 0) return run_tp<DP, 0, true, false, false, 2, false>(VC_TP_ARGS);
-    if (poly == 2) return run_tp<DP, 2, true, false, false, 2, false>(VC_TP_ARGS);
-    if (poly == 3) return run_tp<DP, 3, true, false, false, 2, false>(VC_TP_ARGS);
-    if (poly == 6) return run_tp<DP, 6, true, false, false, 2, false>(VC_TP_ARGS);
-    if (poly == 8) return run_tp<DP, 8, true, false, false, 2, false>(VC_TP_ARGS);
+    if (poly == 0) return run_tp<DP, 0, true, false, false, 2, true>(VC_TP_ARGS);
+    if (poly == 2) return run_tp<DP, 2, true, false, false, 2, true>(VC_TP_ARGS);
+    if (poly == 3) return run_tp<DP, 3, true, false, false, 2, true>(VC_TP_ARGS);
+    if (poly == 6) return run_tp<DP, 6, true, false, false, 2, true>(VC_TP_ARGS);
+    if (poly == 8) return run_tp<DP, 8, true, false, false, 2, true>(VC_TP_ARGS);
   }
 #endif
 #define VC_TP_PICK(ON)                                                                                   \
