@@ -432,18 +432,23 @@ int launch_pack(const float* raw, void* wqkv, float* bias, void* wo, int D, int 
 
 // V^T rows [dh, DP) of every (sequence, head) slot for keys [0, keys): the
 // ones column (row dh) and zeros.  The compact QKV GEMM writes rows < dh only.
+// 16-byte stores over whole rows when the pitch allows (keys past `keys` up
+// to the pitch are never read: the attention's V map ends at Lk).
+template <bool V16>
 __global__ void fill_vt_pad_kernel(__nv_bfloat16* __restrict__ vt, int64_t nslots, int DP, int dh, int64_t ld,
                                    int64_t keys) {
   const int rows = DP - dh;
-  const int64_t kw = (keys + 1) / 2;  // 4-byte words per row (ld even)
+  const int64_t kw = V16 ? ld / 8 : (keys + 1) / 2;  // vectors per row
   const int64_t total = nslots * rows * kw;
-  const __nv_bfloat162 one = __floats2bfloat162_rn(1.f, 1.f), zero = __floats2bfloat162_rn(0.f, 0.f);
+  const uint32_t one2 = 0x3f803f80u;  // bf16x2 (1, 1)
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t w = e % kw;
     const int64_t sr = e / kw;
     const int r = (int)(sr % rows);
     const int64_t slot = sr / rows;
-    reinterpret_cast<__nv_bfloat162*>(vt + (slot * DP + dh + r) * ld)[w] = r == 0 ? one : zero;
+    const uint32_t x = r == 0 ? one2 : 0u;
+    if (V16) reinterpret_cast<uint4*>(vt + (slot * DP + dh + r) * ld)[w] = make_uint4(x, x, x, x);
+    else reinterpret_cast<uint32_t*>(vt + (slot * DP + dh + r) * ld)[w] = x;
   }
 }
 
@@ -451,8 +456,11 @@ int launch_fill_vt_pad(__nv_bfloat16* vt, int64_t nslots, int DP, int dh, int64_
                        cudaStream_t st) {
   if (nslots <= 0 || keys <= 0 || dh >= DP) return VC_OK;
   if (ld % 2) { set_error("V^T pitch must be even"); return VC_EINVAL; }
-  const int64_t total = nslots * (DP - dh) * ((keys + 1) / 2);
-  fill_vt_pad_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 16), 256, 0, st>>>(vt, nslots, DP, dh, ld, keys);
+  const bool v16 = ld % 8 == 0 && ((uintptr_t)vt % 16) == 0;
+  const int64_t total = nslots * (DP - dh) * (v16 ? ld / 8 : (keys + 1) / 2);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+  if (v16) fill_vt_pad_kernel<true><<<blocks, 256, 0, st>>>(vt, nslots, DP, dh, ld, keys);
+  else fill_vt_pad_kernel<false><<<blocks, 256, 0, st>>>(vt, nslots, DP, dh, ld, keys);
   VC_CHECK_LAUNCH();
   return VC_OK;
 }

@@ -22,7 +22,7 @@ for step in "$@"; do
     launches) run 300 launches ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
            --log-file "gpurun_out/${TAG}_launches.csv" python bench.py --steps 2 --warmup 3 --no-cpu-baseline ;;
     ncufull) run 900 ncufull ncu --set full --clock-control none --import-source on \
-           -k regex:"ln_rows|gemm_tc|attn_tc|temporal" -c 8 -o "gpurun_out/${TAG}_block" python tools/run_block.py --iters 1 ;;
+           -k regex:"ln_rows|gemm_tc|attn_t|temporal" -c 10 -o "gpurun_out/${TAG}_block" python tools/run_block.py --iters 1 ;;
     ext) run 300 ext python tools/ext_bench.py ;;
     cfg*) run 600 "$step" python bench.py --config "${step#cfg}" --no-cpu-baseline ;;
     py:*) run 900 "$(echo "${step#py:}" | tr -c 'a-zA-Z0-9_\n' '_' | cut -c1-40)" python ${step#py:} ;;
