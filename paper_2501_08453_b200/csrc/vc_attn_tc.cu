@@ -355,19 +355,23 @@ int launch_attn_tc(const AttnTcParams& p, const void* q, const void* k, const vo
   if (p.Lq <= 0 || nseq <= 0) return VC_OK;
   if (p.Lk <= 0) { set_error("attention needs at least one key"); return VC_EINVAL; }
   if (nseq > 65535 || p.H > 65535) { set_error("attention grid too large"); return VC_ENOTSUP; }
-  // DP <= 80 (the 2B head dim 66 -> 80, dh 64): the two-tile split-row
-  // kernel (vc_attn_tc3.cu); DP = 128: the one-tile kernel above.  Variants
-  // measured slower in round 1 are in git history
-  // (profiles/r01/attn_study/README.md).
+  // DP <= 80 (the 2B head dim 66 -> 80, dh 64): attn_tp_kernel (P in TMEM,
+  // split-row fixed-offset softmax, vc_attn_tp.cu); DP = 128: the one-tile
+  // kernel above.  Variants measured slower are in git history or tuning
+  // builds (profiles/r01/attn_study, profiles/r02/attn).
   // VC_ATTN_IMPL (tuning builds): 3 = the round-1 split-row kernel with half
   // of P in shared memory; default 4 = P entirely in TMEM (vc_attn_tp.cu)
   static const int impl = tuning_int("VC_ATTN_IMPL", 4);
   switch (DP) {
     case 64:
+#ifdef VC_TUNING
       if (impl == 3) return launch_attn_tc3<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+#endif
       return launch_attn_tp<64>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 80:
+#ifdef VC_TUNING
       if (impl == 3) return launch_attn_tc3<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
+#endif
       return launch_attn_tp<80>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
     case 128: return launch_dp<128>(p, q, k, vt, nseq, q_rows_per_seq, k_rows_per_seq, ld_key, st);
   }

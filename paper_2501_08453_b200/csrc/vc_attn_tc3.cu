@@ -17,6 +17,10 @@
 //   * four softmax warps per sub-partition hide each other's latencies.
 // 18 warps: w0 TMA producer, w1 MMA issuer + TMEM owner, w2..w17 softmax
 // (w = 2 + 8*tile + 4*half + i; w % 4 is the TMEM lane quarter).
+// Tuning builds only (-DVC_TUNING, VC_ATTN_IMPL=3): the round-1 kernel kept
+// as the A/B reference of profiles/r02/attn/README.md; the product library
+// does not contain it.
+#ifdef VC_TUNING
 #include "vc_attn_tc_common.cuh"
 #include "vc_tuning.h"
 
@@ -482,3 +486,4 @@ template int launch_attn_tc3<80>(const AttnTcParams&, const void*, const void*, 
                                  int64_t, int64_t, cudaStream_t);
 
 }  // namespace vc
+#endif  // VC_TUNING

@@ -453,7 +453,9 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
   static const int poly = tuning_int("VC_POLY_EVERY", 4);
   static const int narrow_on = tuning_int("VC_ATTN_NARROW", 0);
   static const int fr = tuning_int("VC_ATTN_FR", 0);
-  if (DP == 80 && ones && p.dh < 72 && narrow_on) return run_tp<80, 4, true, true, false, 2, true>(VC_TP_ARGS);
+  if (DP == 80 && ones && p.dh < 72 && narrow_on == 1) return run_tp<80, 4, true, true, false, 2, true>(VC_TP_ARGS);
+  if (DP == 80 && ones && p.dh < 72 && narrow_on == 2 && nt1)
+    return run_tp<80, 4, true, true, false, 1, true>(VC_TP_ARGS);
   if (fr) return ones ? run_tp<DP, 4, true, false, true, 2, false>(VC_TP_ARGS)
                       : run_tp<DP, 4, false, false, true, 2, false>(VC_TP_ARGS);
   if (poly != 4 && ones) {
