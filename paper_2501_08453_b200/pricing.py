@@ -74,8 +74,8 @@ def price_sp_block(stage_ms: dict, frames: int, visual_len: int, text_len: int, 
                    sp_overhead_ms: float = 0.0) -> dict:
     """Priced time of one block forward on P ranks (slowest rank), from the
     measured single-GPU stage times. sp_overhead_ms: the SP path's extra
-    layout passes (exchange-buffer unpacks) measured at P = 1, divided over
-    the ranks like the activations. Returns ms per block, the exchange bytes
+    layout passes (exchange-buffer unpacks) over the FULL data at one rank;
+    a rank unpacks only its peers' share of its 1/P. Returns ms per block, the exchange bytes
     per rank and the exposed communication."""
     if heads % p:
         raise ValueError(f"head-parallel pricing needs P | H ({p} does not divide {heads})")
@@ -88,8 +88,12 @@ def price_sp_block(stage_ms: dict, frames: int, visual_len: int, text_len: int, 
     # slowest rank's bytes: the one with the most rows sends/receives most
     r_max = max(range(p), key=lambda r: vb[r + 1] - vb[r])
     c = exchange_counts(frames, visual_len, heads, dim, p, r_max)
-    a2a1 = sum(c["send1"]) * 2.0 / 2   # bytes per branch (bf16, branch-major halves)
-    a2a2 = sum(c["recv2"]) * 2.0 / 2
+    # bytes per branch per device as the reference's alpha-beta term counts
+    # them (own block included; (p-1)/p of it crosses the links): the counts
+    # as laid out exclude the own block, which has the size of any peer's
+    other = (r_max + 1) % p
+    a2a1 = (sum(c["send1"]) + c["send1"][other]) * 2.0 / 2   # bf16, branch-major halves
+    a2a2 = (sum(c["recv2"]) + c["recv2"][other]) * 2.0 / 2
     t1 = alltoall_time(p, a2a1, spec.intra_bw, spec.alpha) * 1e3   # ms per branch
     t2 = alltoall_time(p, a2a2, spec.intra_bw, spec.alpha) * 1e3
     comm = 2 * (t1 + t2)
@@ -111,7 +115,8 @@ def price_sp_block(stage_ms: dict, frames: int, visual_len: int, text_len: int, 
         fs_end = max(sp_end, a1_fs) + fs_att
         a2_fs = max(fs_end, a2_sp) + t2
         exposed = a2_fs - (tm + sp_att + fs_att)  # the critical path beyond the compute it overlaps
-    layout = sp_overhead_ms * row_share if p > 1 else 0.0
+    # the unpacks of the peers' share ((p-1)/p of this rank's 1/p of the data)
+    layout = sp_overhead_ms * row_share * (p - 1) / p if p > 1 else 0.0
     total = sum(compute.values()) + layout + exposed
     return {"p": p, "ms": total, "compute_ms": sum(compute.values()) + layout, "comm_ms": comm,
             "exposed_comm_ms": exposed, "a2a1_bytes_per_branch": a2a1, "a2a2_bytes_per_branch": a2a2}
