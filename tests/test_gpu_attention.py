@@ -137,19 +137,22 @@ def test_persistent_variant_matches_oracle(vc):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("sk", [600, 5000])  # one-tile (short) and two-tile CTAs
-def test_bf16_attention_logit_range_across_key_blocks(vc, sk):
+@pytest.mark.parametrize("sk,dh", [(600, 66), (5000, 66), (5000, 64), (700, 128)])
+def test_bf16_attention_logit_range_across_key_blocks(vc, sk, dh):
+    # one-tile (short) and two-tile CTAs of the DP-80 kernel, DP 64 (row sum
+    # on the CUDA cores, no ones column) and the DP-128 one-tile kernel
     # The softmax offset is fixed from the first key block's exact max (+60 in
     # log2 units, vc_attn_tc_common.cuh kFixedMaxMargin): keys of later blocks
     # whose logits lie ~140 log2 units ABOVE every first-block logit must still
     # give the exact softmax (no overflow, no lost mass). Inputs are bf16-exact
     # (20 x multiples of 1/64), so the logits themselves carry no rounding.
-    sq, dh = 200, 66
+    sq = 200
     r = np.random.default_rng(11)
     q = np.zeros((sq, dh)); q[:, 0] = 20.0
     k = np.zeros((sk, dh))
-    k[:112, 0] = -20.0                                           # first block: logits -49 nats
-    k[112:, 0] = 20.0 * r.choice([0.90625, 0.9375, 0.96875, 1.0], sk - 112)  # later: +44..+49 nats
+    nb = 112 if 64 < dh <= 80 else 128  # the kernel's first key block
+    k[:nb, 0] = -20.0                                            # first block: logits -49 nats (dh 66)
+    k[nb:, 0] = 20.0 * r.choice([0.90625, 0.9375, 0.96875, 1.0], sk - nb)  # later: +44..+49 nats
     v = r.standard_normal((sk, dh))
     got = vc.attention(q, k, v, 1, dtype="bf16")
     ref = O.attention(q, k, v, 1)
