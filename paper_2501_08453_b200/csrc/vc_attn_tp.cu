@@ -81,20 +81,21 @@ __device__ unsigned long long g_attn_cta[16384][5];
 // NT: query tiles per CTA. NT = 1 (short sequences: the spatial branch):
 // 256 TMEM columns and a 2-deep K / V ring, so two CTAs share an SM and one's
 // prologue / epilogue runs under the other's main loop.
-template <int DP, bool NARROW = false, bool FR = false, int NT = 2>
+// NARROW 2 (DP 80, dh <= 71): 112-key blocks with O in 72 columns (P.V N = 72).
+template <int DP, int NARROW = 0, bool FR = false, int NT = 2>
 struct CfgTp {
   static constexpr int N64 = DP / 64;
   static constexpr int TAIL = DP % 64;
   static_assert(TAIL == 0 || TAIL == 16, "DP must be 64*n or 64*n+16");
   static_assert(DP <= 80, "S + P + O must fit 256 TMEM columns per tile");
   static_assert(!NARROW || DP == 80, "the narrow layout is the DP 80 one");
-  static constexpr int BK = NARROW ? 120 : DP == 64 ? 128 : 112;  // keys per block
+  static constexpr int BK = NARROW == 1 ? 120 : DP == 64 ? 128 : 112;  // keys per block
   static constexpr int HK = FR ? BK : BK / 2;                     // keys per softmax thread
   static constexpr int WARPS = FR ? 4 + 4 * NT : 3 + 8 * NT;
   static constexpr int TMEM_COLS = 256 * NT;
   static constexpr int SM0 = FR ? 4 : 3;                          // first softmax warp
   static constexpr int SM_ARRIVALS = FR ? 128 : 256;              // softmax threads per tile
-  static constexpr int PKEYS = NARROW ? 128 : BK;                 // the P.V K extent
+  static constexpr int PKEYS = NARROW == 1 ? 128 : BK;            // the P.V K extent
   static constexpr int ON = NARROW ? 72 : DP;                     // O columns
   static constexpr int SCOL = 0, PCOL = BK, OCOL = BK + PKEYS / 2;
   static_assert(OCOL + ON <= 256, "per-tile TMEM columns");
@@ -115,7 +116,7 @@ struct CfgTp {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, int POLY, bool ONES, bool NARROW, bool FR = false, int NT = 2, bool FIXM = false>
+template <int DP, int POLY, bool ONES, int NARROW, bool FR = false, int NT = 2, bool FIXM = false>
 __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR, NT>::WARPS * 32, NT == 1 ? 2 : 1)
     attn_tp_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
@@ -415,7 +416,7 @@ int attn_cta_read(unsigned long long* host) {  // [16384][5]
 #endif
 
 // One launch of a kernel variant (maps built with its key-block rows).
-template <int DP, int POLY, bool ONES, bool NARROW, bool FR, int NT, bool FIXM>
+template <int DP, int POLY, bool ONES, int NARROW, bool FR, int NT, bool FIXM>
 int run_tp(const AttnTcParams& p, const void* q, const void* k, const void* vt, int nseq, int64_t q_rows_per_seq,
            int64_t k_rows_per_seq, int64_t ld_key, cudaStream_t st) {
   using CF = CfgTp<DP, NARROW, FR, NT>;
@@ -448,14 +449,18 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
   // 2.84 ms, spatial 0.320 -> 0.287 ms at config 2 (tools/ab_bench.sh, 3
   // rounds). VC_ATTN_FIXM=0: the lazy-rescale online softmax.
   static const int fixm = tuning_int("VC_ATTN_FIXM", 1);
+  // P.V into a 72-column O when dh + the ones column fit (dh <= 71): 10%
+  // less P.V work (full sequence 2.859 vs 2.872 ms, 3 rounds). VC_ATTN_NARROW:
+  // 2 this (default), 0 the 80-column O, 1 120-key blocks as well (dropped)
+  static const int narrow_on = tuning_int("VC_ATTN_NARROW", 2);
+  const bool o72 = DP == 80 && ones && p.dh < 72 && narrow_on == 2 && fixm;
+  if (o72) return nt1 ? run_tp<80, 4, true, 2, false, 1, true>(VC_TP_ARGS)
+                      : run_tp<80, 4, true, 2, false, 2, true>(VC_TP_ARGS);
 #ifdef VC_TUNING
   // measured-and-dropped variants (profiles/r02/attn/README.md): tuning builds only
   static const int poly = tuning_int("VC_POLY_EVERY", 4);
-  static const int narrow_on = tuning_int("VC_ATTN_NARROW", 0);
   static const int fr = tuning_int("VC_ATTN_FR", 0);
-  if (DP == 80 && ones && p.dh < 72 && narrow_on == 1) return run_tp<80, 4, true, true, false, 2, true>(VC_TP_ARGS);
-  if (DP == 80 && ones && p.dh < 72 && narrow_on == 2 && nt1)
-    return run_tp<80, 4, true, true, false, 1, true>(VC_TP_ARGS);
+  if (DP == 80 && ones && p.dh < 72 && narrow_on == 1) return run_tp<80, 4, true, 1, false, 2, true>(VC_TP_ARGS);
   if (fr) return ones ? run_tp<DP, 4, true, false, true, 2, false>(VC_TP_ARGS)
                       : run_tp<DP, 4, false, false, true, 2, false>(VC_TP_ARGS);
   if (poly != 4 && ones) {
