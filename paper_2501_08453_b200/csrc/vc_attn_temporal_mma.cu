@@ -21,6 +21,7 @@ namespace vc {
 namespace {
 
 constexpr int kWarps = 4;
+constexpr float kFixedMargin = 60.0f;  // = attn::kFixedMaxMargin (vc_attn_tc_common.cuh)
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -185,45 +186,38 @@ __global__ void __launch_bounds__(SHARED ? kWarpsShared * 32 : kWarps * 32, SHAR
         mma_bf16_16816(s[nt], qa[ks], b0, b1);
       }
     }
-    // ---- online softmax (rows g and g+8 of the tile; keys past F masked) ----
-    float bm0 = -INFINITY, bm1 = -INFINITY;
+    // ---- softmax (rows g and g+8 of the tile; keys past F masked) with the
+    //      fixed offset of the tc kernels (vc_attn_tc_common.cuh
+    //      kFixedMaxMargin): the first key block's exact row max + 60, then
+    //      no per-block max, shuffles or O rescale ----
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int key = k0 + 8 * nt + 2 * t + i;
-        const bool ok = key < F;
+        const bool ok = k0 + 8 * nt + 2 * t + i < F;
         s[nt][i] = ok ? s[nt][i] * scale_log2 : -INFINITY;
         s[nt][2 + i] = ok ? s[nt][2 + i] * scale_log2 : -INFINITY;
-        bm0 = fmaxf(bm0, s[nt][i]);
-        bm1 = fmaxf(bm1, s[nt][2 + i]);
       }
     }
-    bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
-    bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
-    bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
-    bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
-    const float mn0 = fmaxf(m0, bm0), mn1 = fmaxf(m1, bm1);
-    const float a0 = ptx::ex2(m0 - mn0), a1 = ptx::ex2(m1 - mn1);  // 0 on the first block
-    m0 = mn0;
-    m1 = mn1;
-    float rs0 = 0.f, rs1 = 0.f;
+    if (k0 == 0) {
+      float bm0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+      float bm1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+      bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
+      bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+      bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
+      bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+      m0 = bm0 + kFixedMargin;
+      m1 = bm1 + kFixedMargin;
+    }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        s[nt][i] = ptx::ex2(s[nt][i] - mn0);
-        s[nt][2 + i] = ptx::ex2(s[nt][2 + i] - mn1);
-        rs0 += s[nt][i];
-        rs1 += s[nt][2 + i];
+        s[nt][i] = ptx::ex2(s[nt][i] - m0);
+        s[nt][2 + i] = ptx::ex2(s[nt][2 + i] - m1);
+        l0 += s[nt][i];  // per-thread partial sums; reduced over the quad at the end
+        l1 += s[nt][2 + i];
       }
-    }
-    l0 = l0 * a0 + rs0;  // per-thread partial sums; reduced over the quad at the end
-    l1 = l1 * a1 + rs1;
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      oacc[j][0] *= a0; oacc[j][1] *= a0;
-      oacc[j][2] *= a1; oacc[j][3] *= a1;
     }
     // ---- O += P V (P from the S accumulators, bf16 A fragment) ----
     uint32_t pa[4];
