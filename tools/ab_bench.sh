@@ -7,7 +7,7 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 TAG=$1; ROUNDS=$2; shift 2
-python -m paper_2501_08453_b200.build --force --tuning > "gpurun_out/${TAG}_build.log" 2>&1 || { echo build failed; exit 1; }
+[ -n "$AB_NOBUILD" ] || python -m paper_2501_08453_b200.build --force --tuning > "gpurun_out/${TAG}_build.log" 2>&1 || { echo build failed; exit 1; }
 for r in $(seq "$ROUNDS"); do
   for v in "$@"; do
     env $v timeout 300 python bench.py --no-cpu-baseline --steps 20 ${AB_ARGS:-} 2>/dev/null | python -c "
