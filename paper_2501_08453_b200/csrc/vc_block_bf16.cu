@@ -45,6 +45,32 @@ WsBf16 ws_layout(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
   w.total = o;
   return w;
 }
+
+// The temporal branch runs on a side stream forked after the QKV GEMM and
+// joined before the O GEMM, so its (memory-bound) CTAs fill the SMs the
+// attention kernels leave idle in their last waves. One side stream and two
+// events per host thread and device (fork / join by events: stream-capture
+// safe). Sequential while the stage profiler runs (per-stage times).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int dev = -1;
+};
+int side_stream(SideStream** out) {
+  static thread_local SideStream ss[16];
+  int dev = 0;
+  VC_CHECK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) { set_error("device %d out of range", dev); return VC_EINVAL; }
+  SideStream& x = ss[dev];
+  if (!x.s) {
+    VC_CHECK_CUDA(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
+    VC_CHECK_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
+    VC_CHECK_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
+    x.dev = dev;
+  }
+  *out = &x;
+  return VC_OK;
+}
 }  // namespace
 
 size_t bf16_workspace_bytes(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
@@ -129,6 +155,16 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   if (slot) wo = wo_s;
   const int64_t bw = slot ? H * slot : D;  // columns per branch in acat
   const int64_t lda = 3 * bw;
+  // temporal branch on the side stream (forked here, joined before the O GEMM)
+  static const int fork_on = tuning_int("VC_TEMPORAL_FORK", 1);
+  SideStream* side = nullptr;
+  if (fork_on && !profile_on()) {
+    VC_TRY(side_stream(&side));
+    VC_CHECK_CUDA(cudaEventRecord(side->fork, st));
+    VC_CHECK_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+    VC_TRY(launch_temporal_bf16(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, side->s, slot, 1));
+    VC_CHECK_CUDA(cudaEventRecord(side->join, side->s));
+  }
   {
     AttnTcParams a{};
     a.Lq = (int)Lv; a.Lk = (int)Lv; a.H = (int)H; a.dh = (int)dh;
@@ -137,8 +173,10 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_attn_tc(a, sc.sp.q, sc.sp.k, sc.sp.vt, (int)F, Lv, Lv, wl.Lv_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_spatial");
-  VC_TRY(launch_temporal_bf16(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, st, slot, 1));
-  profile_mark(st, "attn_temporal");
+  if (!side) {
+    VC_TRY(launch_temporal_bf16(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, st, slot, 1));
+    profile_mark(st, "attn_temporal");
+  }
   {
     AttnTcParams a{};
     a.Lq = (int)Nv; a.Lk = (int)(Lt + Nv); a.H = (int)H; a.dh = (int)dh;
@@ -147,6 +185,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_attn_tc(a, sc.fs.q, sc.fs.k, sc.fs.vt, 1, Nv, Lt + Nv, wl.Lk_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_fullseq");
+  if (side) VC_CHECK_CUDA(cudaStreamWaitEvent(st, side->join, 0));
   if (ext) {  // h = x + gate_msa * (branch sum)  -> out
     GemmTcParams g{};
     g.M = Nv; g.N = (int)D; g.K = (int)(3 * D);
