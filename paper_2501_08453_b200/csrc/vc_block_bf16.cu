@@ -46,14 +46,15 @@ WsBf16 ws_layout(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H) {
   return w;
 }
 
-// The temporal branch runs on a side stream forked after the QKV GEMM and
-// joined before the O GEMM, so its (memory-bound) CTAs fill the SMs the
-// attention kernels leave idle in their last waves. One side stream and two
+// The text K/V GEMM and the temporal branch run on a side stream forked
+// after the QKV GEMM (joined before the full-sequence attention / the O
+// GEMM), so their CTAs fill the SMs the attention kernels leave idle in their
+// last waves. One side stream and two
 // events per host thread and device (fork / join by events: stream-capture
 // safe). Sequential while the stage profiler runs (per-stage times).
 struct SideStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, text = nullptr, join = nullptr;
   int dev = -1;
 };
 int side_stream(SideStream** out) {
@@ -65,6 +66,7 @@ int side_stream(SideStream** out) {
   if (!x.s) {
     VC_CHECK_CUDA(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
     VC_CHECK_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
+    VC_CHECK_CUDA(cudaEventCreateWithFlags(&x.text, cudaEventDisableTiming));
     VC_CHECK_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
     x.dev = dev;
   }
@@ -140,14 +142,6 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_fill_vt_pad(sc.fs.vt, H, (int)wl.DP, (int)dh, wl.Lk_ld, Lt + Nv, st));
   }
   profile_mark(st, "qkv_gemm");
-  if (Lt > 0) {  // prompt rows: only the full-sequence K and V segments
-    const int64_t n0 = pad.fs_base() + pad.SEG;
-    GemmTcParams g{};
-    g.M = Lt; g.N = (int)(2 * pad.SEG); g.K = (int)D; g.bias = bias + n0;
-    g.qkv = sc; g.qkv.n_base = n0; g.qkv.text_rows = 1;
-    VC_TRY(launch_gemm_tc(xhat + Nv * D, D, (const bf*)wqkv + n0 * D, D, g, qkv_epi, st));
-    profile_mark(st, "text_kv_gemm");
-  }
   const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)dh));
   // O-GEMM A operand: the three branches' outputs [Nv][3D], or, with the
   // head-slot Wo (dh 66), [Nv][3][H][DP] written as whole 16-byte sectors
@@ -155,13 +149,25 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
   if (slot) wo = wo_s;
   const int64_t bw = slot ? H * slot : D;  // columns per branch in acat
   const int64_t lda = 3 * bw;
-  // temporal branch on the side stream (forked here, joined before the O GEMM)
+  // text K/V GEMM and temporal branch on the side stream (forked here)
   static const int fork_on = tuning_int("VC_TEMPORAL_FORK", 1);
   SideStream* side = nullptr;
   if (fork_on && !profile_on()) {
     VC_TRY(side_stream(&side));
     VC_CHECK_CUDA(cudaEventRecord(side->fork, st));
     VC_CHECK_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+  }
+  cudaStream_t sx = side ? side->s : st;
+  if (Lt > 0) {  // prompt rows: only the full-sequence K and V segments
+    const int64_t n0 = pad.fs_base() + pad.SEG;
+    GemmTcParams g{};
+    g.M = Lt; g.N = (int)(2 * pad.SEG); g.K = (int)D; g.bias = bias + n0;
+    g.qkv = sc; g.qkv.n_base = n0; g.qkv.text_rows = 1;
+    VC_TRY(launch_gemm_tc(xhat + Nv * D, D, (const bf*)wqkv + n0 * D, D, g, qkv_epi, sx));
+    if (!side) profile_mark(st, "text_kv_gemm");
+  }
+  if (side) {
+    VC_CHECK_CUDA(cudaEventRecord(side->text, side->s));
     VC_TRY(launch_temporal_bf16(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, side->s, slot, 1));
     VC_CHECK_CUDA(cudaEventRecord(side->join, side->s));
   }
@@ -173,6 +179,7 @@ int block_forward_bf16(int64_t F, int64_t Lv, int64_t Lt, int64_t D, int64_t H, 
     VC_TRY(launch_attn_tc(a, sc.sp.q, sc.sp.k, sc.sp.vt, (int)F, Lv, Lv, wl.Lv_ld, (int)wl.DP, st));
   }
   profile_mark(st, "attn_spatial");
+  if (side) VC_CHECK_CUDA(cudaStreamWaitEvent(st, side->text, 0));  // the text keys of the full sequence
   if (!side) {
     VC_TRY(launch_temporal_bf16(tm, 3 * D, D, acat + bw, lda, (int)F, (int)Lv, (int)H, (int)dh, st, slot, 1));
     profile_mark(st, "attn_temporal");
