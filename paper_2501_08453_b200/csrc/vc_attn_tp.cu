@@ -454,6 +454,16 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
   // 2 this (default), 0 the 80-column O, 1 120-key blocks as well (dropped)
   static const int narrow_on = tuning_int("VC_ATTN_NARROW", 2);
   const bool o72 = DP == 80 && ones && p.dh < 72 && narrow_on == 2 && fixm;
+#ifdef VC_TUNING
+  static const int poly72 = tuning_int("VC_POLY_EVERY", 4);
+  if (o72 && poly72 != 4) {  // exp-offload ratio A/B on the default layout
+#define VC_TP_POLY(PV) \
+    if (poly72 == PV) return nt1 ? run_tp<80, PV, true, 2, false, 1, true>(VC_TP_ARGS) \
+                                 : run_tp<80, PV, true, 2, false, 2, true>(VC_TP_ARGS);
+    VC_TP_POLY(0) VC_TP_POLY(3) VC_TP_POLY(6)
+#undef VC_TP_POLY
+  }
+#endif
   if (o72) return nt1 ? run_tp<80, 4, true, 2, false, 1, true>(VC_TP_ARGS)
                       : run_tp<80, 4, true, 2, false, 2, true>(VC_TP_ARGS);
 #ifdef VC_TUNING
