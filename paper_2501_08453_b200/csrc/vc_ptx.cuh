@@ -442,6 +442,20 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __uint_as_float(__float_as_uint(qq.y) + (__float_as_uint(tt.y) << 23)));
 }
 
+// degree-2 variant (max relative error 1.7e-3, below a bf16 P's rounding step)
+__device__ __forceinline__ float2 ex2_poly2_d2(float2 x) {
+  const unsigned long long xx = pk2(make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f)));
+  unsigned long long t, j, f, q;
+  asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(t) : "l"(xx), "l"(pk2(12582912.f)));
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(j) : "l"(t), "l"(pk2(-12582912.f)));
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(f) : "l"(xx), "l"(j));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(q) : "l"(f), "l"(pk2(0.33718041f)), "l"(pk2(0.65762907f)));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(q) : "l"(q), "l"(f), "l"(pk2(1.00173f)));
+  const float2 tt = up2(t), qq = up2(q);
+  return make_float2(__uint_as_float(__float_as_uint(qq.x) + (__float_as_uint(tt.x) << 23)),
+                     __uint_as_float(__float_as_uint(qq.y) + (__float_as_uint(tt.y) << 23)));
+}
+
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
