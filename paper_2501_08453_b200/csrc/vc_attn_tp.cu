@@ -344,8 +344,13 @@ __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR, NT>::WARPS * 32, NT == 1
 #pragma unroll
         for (int i = 0; i < HK; i += 2) {
           float2 e = ptx::ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nm2);
-          constexpr int PR = POLY % 100;  // POLY >= 100: the degree-2 polynomial, 1 pair in POLY - 100
-          if (PR > 0 && ((i >> 1) % (PR > 0 ? PR : 1)) == PR - 1) {
+          // POLY >= 100: the degree-2 polynomial on 1 pair in POLY % 100; 2xx: on
+          // 2 pairs in POLY % 100 (pair indices 1 and 3 of each group)
+          constexpr int PR = POLY % 100;
+          constexpr int PG = PR > 0 ? PR : 1;
+          const bool off = POLY >= 200 ? (((i >> 1) % PG) == 1 || ((i >> 1) % PG) == 3)
+                                       : (PR > 0 && ((i >> 1) % PG) == PR - 1);
+          if (off) {
             e = POLY >= 100 ? ptx::ex2_poly2_d2(e) : ptx::ex2_poly2(e);
           } else {
             e.x = ptx::ex2(e.x);
@@ -455,21 +460,22 @@ int launch_attn_tp(const AttnTcParams& p, const void* q, const void* k, const vo
   // 2 this (default), 0 the 80-column O, 1 120-key blocks as well (dropped)
   static const int narrow_on = tuning_int("VC_ATTN_NARROW", 2);
   const bool o72 = DP == 80 && ones && p.dh < 72 && narrow_on == 2 && fixm;
-  // exponentials: 1 pair in 3 on the FMA pipe as a degree-2 polynomial
+  // exponentials: 2 pairs in 7 on the FMA pipe as a degree-2 polynomial
   // (ex2_poly2_d2, error below a bf16 P's rounding step): full sequence
-  // 2.822 vs 2.85 ms for the cubic on 1 pair in 4 (3 rounds; no offload 3.16)
+  // 2.807 ms vs 2.817 for 1 pair in 3, 2.85 for the cubic on 1 in 4, 2.91
+  // for 2 in 5 (3 rounds each; no offload 3.16)
 #ifdef VC_TUNING
-  static const int poly72 = tuning_int("VC_POLY_EVERY", 103);
-  if (o72 && poly72 != 103) {  // exp-offload A/B on the default layout
+  static const int poly72 = tuning_int("VC_POLY_EVERY", 207);
+  if (o72 && poly72 != 207) {  // exp-offload A/B on the default layout
 #define VC_TP_POLY(PV) \
     if (poly72 == PV) return nt1 ? run_tp<80, PV, true, 2, false, 1, true>(VC_TP_ARGS) \
                                  : run_tp<80, PV, true, 2, false, 2, true>(VC_TP_ARGS);
-    VC_TP_POLY(0) VC_TP_POLY(3) VC_TP_POLY(4) VC_TP_POLY(6) VC_TP_POLY(104) VC_TP_POLY(102)
+    VC_TP_POLY(0) VC_TP_POLY(3) VC_TP_POLY(4) VC_TP_POLY(6) VC_TP_POLY(103) VC_TP_POLY(104) VC_TP_POLY(102) VC_TP_POLY(205)
 #undef VC_TP_POLY
   }
 #endif
-  if (o72) return nt1 ? run_tp<80, 103, true, 2, false, 1, true>(VC_TP_ARGS)
-                      : run_tp<80, 103, true, 2, false, 2, true>(VC_TP_ARGS);
+  if (o72) return nt1 ? run_tp<80, 207, true, 2, false, 1, true>(VC_TP_ARGS)
+                      : run_tp<80, 207, true, 2, false, 2, true>(VC_TP_ARGS);
 #ifdef VC_TUNING
   // measured-and-dropped variants (profiles/r02/attn/README.md): tuning builds only
   static const int poly = tuning_int("VC_POLY_EVERY", 4);
