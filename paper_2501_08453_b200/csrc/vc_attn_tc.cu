@@ -53,7 +53,9 @@ struct Cfg {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int DP, bool FIXM>
+// POLY: exp pairs on the FMA-pipe polynomial (0 none; 207: degree 2 on 2
+// pairs in 7, as attn_tp_kernel; 103: degree 2 on 1 pair in 3)
+template <int DP, bool FIXM, int POLY = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ64, const __grid_constant__ CUtensorMap tmQ16,
                    const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmK16,
@@ -236,8 +238,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int i = 0; i < BKV; i += 2) {
         float2 t = ptx::ffma2(make_float2(v[i], v[i + 1]), sc2, nm2);
-        t.x = ptx::ex2(t.x);
-        t.y = ptx::ex2(t.y);
+        constexpr int PG = POLY % 100 > 0 ? POLY % 100 : 1;
+        const bool off = POLY >= 200 ? (((i >> 1) % PG) == 1 || ((i >> 1) % PG) == 3)
+                                     : (POLY > 0 && ((i >> 1) % PG) == PG - 1);
+        if (off) {
+          t = ptx::ex2_poly2_d2(t);
+        } else {
+          t.x = ptx::ex2(t.x);
+          t.y = ptx::ex2(t.y);
+        }
         v[i] = t.x;
         v[i + 1] = t.y;
         s4[(i >> 1) & 3] = ptx::fadd2(s4[(i >> 1) & 3], t);
@@ -328,11 +337,16 @@ int launch_dp(const AttnTcParams& p, const void* q, const void* k, const void* v
   // fixed-offset softmax after the first key tile (vc_attn_tc_common.cuh
   // kFixedMaxMargin); VC_ATTN_FIXM=0: lazy rescale
   static const int fixm = tuning_int("VC_ATTN_FIXM", 1);
-  auto kern = fixm ? attn_tc_kernel<DP, true> : attn_tc_kernel<DP, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[fixm ? 1 : 0]) {
+  // exp offload onto the FMA pipe (this kernel has one softmax warp per SM
+  // sub-partition, 128 exponentials per row per block: MUFU-bound)
+  static const int poly = tuning_int("VC_ATTN128_POLY", 207);
+  auto kern = !fixm ? attn_tc_kernel<DP, false> : poly == 207 ? attn_tc_kernel<DP, true, 207>
+            : poly == 103 ? attn_tc_kernel<DP, true, 103> : attn_tc_kernel<DP, true, 0>;
+  static bool attr[4] = {false, false, false, false};
+  const int ai = !fixm ? 0 : poly == 207 ? 1 : poly == 103 ? 2 : 3;
+  if (!attr[ai]) {
     VC_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
-    attr[fixm ? 1 : 0] = true;
+    attr[ai] = true;
   }
   dim3 grid((unsigned)cdiv(p.Lq, BQ), (unsigned)p.H, (unsigned)nseq);
   kern<<<grid, kThreads, CF::SMEM, st>>>(mq64, mq16, mk64, mk16, mv, p);
