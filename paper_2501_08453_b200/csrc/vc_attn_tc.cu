@@ -338,12 +338,18 @@ int launch_dp(const AttnTcParams& p, const void* q, const void* k, const void* v
   // kFixedMaxMargin); VC_ATTN_FIXM=0: lazy rescale
   static const int fixm = tuning_int("VC_ATTN_FIXM", 1);
   // exp offload onto the FMA pipe (this kernel has one softmax warp per SM
-  // sub-partition, 128 exponentials per row per block: MUFU-bound)
-  static const int poly = tuning_int("VC_ATTN128_POLY", 207);
-  auto kern = !fixm ? attn_tc_kernel<DP, false> : poly == 207 ? attn_tc_kernel<DP, true, 207>
-            : poly == 103 ? attn_tc_kernel<DP, true, 103> : attn_tc_kernel<DP, true, 0>;
-  static bool attr[4] = {false, false, false, false};
-  const int ai = !fixm ? 0 : poly == 207 ? 1 : poly == 103 ? 2 : 3;
+  // sub-partition, 128 exponentials per row per block: MUFU-bound): degree-2
+  // polynomial on 2 pairs in 5 (config 5 full sequence 3.03 ms vs 3.11 for 2
+  // in 7, 3.09 for 1 in 2, 3.37 without offload; 3 rounds, tools/ab_bench.sh)
+  static const int poly = tuning_int("VC_ATTN128_POLY", 205);
+  auto kern = !fixm ? attn_tc_kernel<DP, false> : poly == 205 ? attn_tc_kernel<DP, true, 205>
+#ifdef VC_TUNING
+            : poly == 207 ? attn_tc_kernel<DP, true, 207> : poly == 102 ? attn_tc_kernel<DP, true, 102>
+            : poly == 103 ? attn_tc_kernel<DP, true, 103>
+#endif
+            : attn_tc_kernel<DP, true, 0>;
+  static bool attr[6] = {false, false, false, false, false, false};
+  const int ai = !fixm ? 0 : poly == 205 ? 1 : poly == 207 ? 2 : poly == 102 ? 4 : poly == 103 ? 5 : 3;
   if (!attr[ai]) {
     VC_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr[ai] = true;
