@@ -68,7 +68,7 @@ int main(int argc, char** argv) {
   if (getenv("VC_TRACE_CTA")) {  // per-CTA phases of the LAST launch, per-SM gaps between CTAs
     std::vector<unsigned long long> c(16384 * 5);
     vc::attn_cta_read(c.data());
-    const int nb = ((Lq + 255) / 256) * H;
+    const int nb = 16384;  // every CTA that stamped (one or two tiles per CTA)
     double pro = 0, main_ = 0, epi = 0, gap = 0;
     int ng = 0, n = 0;
     std::vector<std::vector<std::pair<unsigned long long, unsigned long long>>> sm(256);
