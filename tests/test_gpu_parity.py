@@ -315,3 +315,27 @@ def test_vae_encode_and_fused_q_sample_vs_golden(vc):
         assert normwise(got, G[f"qs37_{h}x{w}_c{c}"]) <= 1e-6
     with pytest.raises(ValueError, match="pixels"):
         vc.toy_vae_encode(np.zeros((8, 8, 4)))
+
+
+def test_block_forward_captures_into_a_cuda_graph(vc):
+    # the bf16 block forks its text K/V GEMM and temporal branch onto a side
+    # stream and joins them back with events (vc_block_bf16.cu): the whole
+    # forward must capture into one CUDA graph and replay to the same bits
+    import torch
+
+    from paper_2501_08453_b200.model import DeviceBlock, block_forward_device
+    blk, x, prompt = block_case(vc, "blk_graph", 3, 40, 8, 264)  # dh 66: compact QKV, pad fills, side stream
+    db = DeviceBlock(torch, blk, 4, "bf16")
+    xt = torch.from_numpy(x.astype(np.float32)).cuda()
+    pt = torch.from_numpy(prompt.astype(np.float32)).cuda()
+    ref = torch.empty_like(xt)
+    block_forward_device(torch, db, xt, pt, ref, False)  # warm: attributes, workspace
+    out = torch.zeros_like(xt)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        block_forward_device(torch, db, xt, pt, out, False)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
