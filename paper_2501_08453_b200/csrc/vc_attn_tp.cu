@@ -185,12 +185,14 @@ __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR, NT>::WARPS * 32, NT == 1
         const uint32_t ph = ((j / KS) & 1) ^ 1;
         const int k0 = j * BK;
         ptx::mbar_wait_sleep(&k_empty[s], ph);
+        VC_TRP(tr, 1, j, 5);  // producer: K(j) issued
         ptx::mbar_arrive_expect_tx(&k_full[s], CF::K_BYTES);
         uint8_t* sK = smem + CF::OFF_K + s * CF::K_STAGE;
         for (int c = 0; c < CF::N64; ++c)
           ptx::tma_load_4d(sK + c * BK * 128, &tmK64, &k_full[s], c * 64, h, k0, seq);
         if (CF::TAIL) ptx::tma_load_4d(sK + CF::N64 * BK * 128, &tmK16, &k_full[s], CF::N64 * 64, h, k0, seq);
         ptx::mbar_wait_sleep(&v_empty[s], ph);
+        VC_TRP(tr, 1, j, 6);  // producer: V(j) issued
         ptx::mbar_arrive_expect_tx(&v_full[s], CF::V_BYTES);
         uint8_t* sV = smem + CF::OFF_V + s * CF::V_BYTES;
         ptx::tma_load_4d(sV, &tmV, &v_full[s], k0, 0, h, seq);
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(CfgTp<DP, NARROW, FR, NT>::WARPS * 32, NT == 1
         if (j + 1 < n_tiles) {  // S(j+1) as soon as the softmax holds S(j) in registers
           const int ks1 = (j + 1) % KS;
           ptx::mbar_wait_sleep(&k_full[ks1], ((j + 1) / KS) & 1);
+          VC_TRP(tr && (threadIdx.x & 31) == 0, t, j, 3);  // K(j+1) landed
           ptx::mbar_wait_sleep(&s_empty[t], j & 1);
           ptx::fence_after_sync();
           if (ptx::elect_one()) mma_s(ks1);
